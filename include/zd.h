@@ -1,0 +1,175 @@
+/*
+ * zd.h — C ABI of the B200-native zd-tree hot path.
+ *
+ * The zd-tree is a kd-tree whose splits follow the Morton (z-order) bit
+ * interleaving (§2 "Data structure"; Blelloch & Dobson,
+ * arXiv 2111.04182).  This library implements, as hand-written sm_100a CUDA
+ * kernels on one GPU:
+ *   zd_build  — Morton encode + radix sort of (key, id) + tree cut at the highest
+ *               differing bit + bottom-up bounding boxes  (§2
+ *               "Construction"; Alg. 1 buildTree P:255-275; empty cuts P:463)
+ *   zd_knn    — all-points exact k-NN graph, leaf-based searchUp/searchDown
+ *               (Alg. 3, Alg. 2, "leaf-based" P:248), or
+ *               external queries located by their Morton bits ("bit-based" P:248)
+ *   zd_insert — batch insert (Alg. 4 batchInsert P:354-377)
+ *   zd_delete — batch delete ("almost identical")
+ *
+ * Domain (fixed universe box; SURVEY.md §8(c) reading 5):
+ *   dim = 2: int32 coordinates with 0 <= c < 2^30  (60-bit Morton keys)
+ *   dim = 3: int32 coordinates with 0 <= c < 2^21  (63-bit Morton keys)
+ * Distances are exact int64 squared Euclidean distances.
+ *
+ * Result semantics (SURVEY §8(c) "Result definition"; readings 13-15, 21):
+ *   row r of an all-points query belongs to the r-th smallest live id; it holds
+ *   the first min(k, L-1) pairs of {(d2(q, p_j), j) : j live, j != id(q)} in
+ *   lexicographic (d2, id) order, padded with (-1, INT64_MAX).  The answer is
+ *   unique, so GPU and oracle rows are compared bit-exactly.
+ *
+ * Pointers: every array argument may be a CUDA device pointer OR a host pointer
+ * (pageable or pinned); the library detects which with
+ * cudaPointerGetAttributes and stages host arrays through device memory itself
+ * (host outputs are complete when the call returns).  Arrays are dense,
+ * row-major, little-endian.  The library copies what it needs from inputs, so the
+ * caller keeps ownership of every buffer it passes and may free it after return.
+ *
+ * Streams: all work runs on the handle's stream (zd_build_ex opts / zd_set_stream;
+ * default: the legacy default stream).  zd_build, zd_insert and zd_delete
+ * synchronize that stream once (to read a validation flag or a count).  zd_knn
+ * with device outputs is asynchronous on the stream.
+ *
+ * Errors: functions returning int/int64 return a negative ZD_E* code on failure;
+ * functions returning pointers return NULL.  zd_last_error() gives a
+ * thread-local message for the most recent failure on the calling thread.
+ * Validation happens before any mutation: a failed insert leaves the tree
+ * unchanged (S:383 all-or-nothing).
+ *
+ * Concurrency: zd_knn may be called concurrently on one handle (read-only);
+ * zd_insert / zd_delete / zd_set_stream / zd_free need exclusive access.
+ */
+#ifndef ZD_H
+#define ZD_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define ZD_API __attribute__((visibility("default")))
+#else
+#define ZD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct zd_tree zd_tree;  /* opaque; owns all device memory it allocates */
+
+enum {
+    ZD_OK = 0,
+    ZD_EINVAL = -1,   /* bad argument (dim, n, k, m, NULL handle, ...) */
+    ZD_ERANGE = -2,   /* a coordinate outside the universe box */
+    ZD_ENOMEM = -3,   /* device allocation failed */
+    ZD_ECUDA = -4     /* any other CUDA runtime error */
+};
+
+#define ZD_K_MAX 32        /* largest k served by zd_knn */
+#define ZD_LEAF_MAX_MAX 32 /* largest leaf size accepted by zd_build_ex */
+
+typedef struct zd_opts {
+    void *stream;   /* cudaStream_t for all work; NULL = legacy default stream */
+    int leaf_max;   /* leaf size bound (reading 1: leaf iff size <= leaf_max or all
+                       keys equal); 0 = default 16; valid 1..ZD_LEAF_MAX_MAX */
+    int timing;     /* nonzero: record per-phase device times (zd_get_timing) */
+} zd_opts;
+
+/* Build a zd-tree over n points (int32 [n][dim]); point i gets id i.
+ * n = 0 is valid (single empty leaf).  Returns NULL on error: dim not in {2,3},
+ * n < 0 or n >= 2^31 (ZD_EINVAL), a coordinate outside the box (ZD_ERANGE),
+ * allocation/CUDA failure.  Cite: Alg. 1 P:255-275. */
+ZD_API zd_tree *zd_build(const int32_t *points, int64_t n, int dim);
+ZD_API zd_tree *zd_build_ex(const int32_t *points, int64_t n, int dim, const zd_opts *opts);
+
+/* Exact k nearest neighbours.
+ *   queries == NULL: all-points k-NN graph over the live points (leaf-based,
+ *     P:248); m must equal zd_size(h); row r = r-th smallest live id (zd_live_ids);
+ *     the query point itself is excluded by id.
+ *   queries != NULL: m external query points int32 [m][dim] inside the box
+ *     (bit-based; "dynamic queries" P:183); row j = query j; nothing excluded.
+ * out_idx: int32 [m][k] neighbour ids; out_dist2: int64 [m][k] squared distances.
+ * 1 <= k <= ZD_K_MAX.  Returns ZD_OK or a negative code (ZD_EINVAL for bad k/m,
+ * ZD_ERANGE for an out-of-box query). */
+ZD_API int zd_knn(zd_tree *h, const int32_t *queries, int64_t m, int k,
+           int32_t *out_idx, int64_t *out_dist2);
+
+/* Insert m points (int32 [m][dim]); they get ids first, first+1, ... where
+ * first = the next unused id (ids are never reused, reading 20).  Returns first
+ * (>= 0) or a negative code; on error the tree is unchanged.  The tree after the
+ * call is the canonical zd-tree of the live multiset (reading 17).  Alg. 4
+ * P:354-377. */
+ZD_API int64_t zd_insert(zd_tree *h, const int32_t *batch, int64_t m);
+
+/* Delete the points with the given ids (int32 [m]).  Absent, already-deleted and
+ * duplicate ids are skipped.  Returns the number of points deleted, or a
+ * negative code.  P:253. */
+ZD_API int64_t zd_delete(zd_tree *h, const int32_t *ids, int64_t m);
+
+/* Number of live points (>= 0), or ZD_EINVAL for a NULL handle. */
+ZD_API int64_t zd_size(const zd_tree *h);
+
+/* Write the live ids in ascending order (int32 [zd_size(h)]) = the row order of
+ * the all-points output (reading 21).  Synchronous. */
+ZD_API int zd_live_ids(const zd_tree *h, int32_t *out);
+
+/* Make all later work on h run on the given cudaStream_t (NULL = legacy default). */
+ZD_API int zd_set_stream(zd_tree *h, void *cuda_stream);
+
+/* Free the handle and all its device memory (NULL is a no-op). */
+ZD_API void zd_free(zd_tree *h);
+
+/* Thread-local message for the last error on this thread ("" if none). */
+ZD_API const char *zd_last_error(void);
+
+/* Thread-local ZD_E* code of the last error on this thread (ZD_OK if none). */
+ZD_API int zd_last_error_code(void);
+
+/* ---- introspection (structural-parity tests and benchmarking) ---------- */
+
+typedef struct zd_info {
+    int dim;
+    int leaf_max;
+    int64_t n;            /* live points */
+    int64_t n_next;       /* next id to be assigned */
+    int64_t n_leaves;     /* leaves of the canonical tree (= n_internal + 1) */
+    int64_t n_internal;   /* internal nodes */
+    int32_t root;         /* root reference: >= 0 internal node, < 0 leaf ~ref */
+    int32_t node_words;   /* int32 words per exported internal node */
+} zd_info;
+
+ZD_API int zd_get_info(const zd_tree *h, zd_info *out);
+
+/* Copy the tree out (synchronous; any pointer may be NULL to skip it):
+ *   keys        uint64 [n]      sorted Morton keys (by key, then id)
+ *   recs        int32 [n][4]    (x, y, z-or-0, id) in the same order
+ *   leaf_start  int32 [n_leaves+1]  leaf l covers sorted positions
+ *                                   [leaf_start[l], leaf_start[l+1])
+ *   leaf_parent int32 [n_leaves]    internal node index, -1 for a root leaf
+ *   nodes       int32 [n_internal][node_words]: internal node i (in-order: it
+ *               separates leaf i from leaf i+1) = left-child box (lo[dim], hi[dim]),
+ *               right-child box (lo[dim], hi[dim]), left ref, right ref, parent,
+ *               split bit.  A ref >= 0 is an internal node, a ref < 0 is leaf ~ref. */
+ZD_API int zd_export(const zd_tree *h, uint64_t *keys, int32_t *recs, int32_t *leaf_start,
+              int32_t *leaf_parent, int32_t *nodes);
+
+/* Per-phase device times (ms, CUDA events on the handle's stream) of the most
+ * recent zd_build / zd_insert / zd_delete / zd_knn call, when enabled by
+ * zd_set_timing(h, 1).  Phases: 0 encode+sort, 1 topology, 2 bbox (bottom-up),
+ * 3 merge/compaction, 4 knn, 5 validation.  Fills min(nphase, 6) entries and
+ * returns the number filled.  Timing adds event records but no extra syncs
+ * beyond the ones each call already makes (zd_knn syncs when timing is on). */
+ZD_API int zd_set_timing(zd_tree *h, int enable);
+ZD_API int zd_get_timing(const zd_tree *h, float *ms, int nphase);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ZD_H */

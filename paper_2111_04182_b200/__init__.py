@@ -1,0 +1,236 @@
+"""B200-native zd-tree (Blelloch & Dobson, arXiv 2111.04182) — Python binding.
+
+Thin ctypes binding over the C ABI in include/zd.h (libzd.so, hand-written sm_100a
+CUDA).  It only marshals arguments: every step of the hot path runs in the CUDA
+kernels.  There is no CPU fallback: if libzd.so is missing or cannot be loaded,
+load() raises.
+
+Arrays may be torch tensors (CUDA or CPU) or numpy arrays; CUDA tensors are passed
+as device pointers, host arrays as host pointers (the library stages them).
+Work runs on torch's current CUDA stream at build time unless a stream is given.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from ._build import LIB_PATH, build_lib
+
+ZD_OK, ZD_EINVAL, ZD_ERANGE, ZD_ENOMEM, ZD_ECUDA = 0, -1, -2, -3, -4
+ZD_K_MAX = 32
+ZD_LEAF_MAX_MAX = 32
+PHASES = ("sort", "topology", "bbox", "merge_compact", "knn", "validate")
+
+_lib = None
+
+
+class ZdError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class _Opts(C.Structure):
+    _fields_ = [("stream", C.c_void_p), ("leaf_max", C.c_int), ("timing", C.c_int)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("dim", C.c_int), ("leaf_max", C.c_int), ("n", C.c_int64), ("n_next", C.c_int64),
+                ("n_leaves", C.c_int64), ("n_internal", C.c_int64), ("root", C.c_int32),
+                ("node_words", C.c_int32)]
+
+
+def load():
+    """Load libzd.so (no rebuild on the GPU box unless sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(f"libzd.so not built ({LIB_PATH}); run __graft_entry__.build()")
+    L = C.CDLL(str(LIB_PATH))
+    P, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+    L.zd_build.restype = P
+    L.zd_build.argtypes = [P, i64, i32]
+    L.zd_build_ex.restype = P
+    L.zd_build_ex.argtypes = [P, i64, i32, C.POINTER(_Opts)]
+    L.zd_knn.restype = i32
+    L.zd_knn.argtypes = [P, P, i64, i32, P, P]
+    L.zd_insert.restype = i64
+    L.zd_insert.argtypes = [P, P, i64]
+    L.zd_delete.restype = i64
+    L.zd_delete.argtypes = [P, P, i64]
+    L.zd_size.restype = i64
+    L.zd_size.argtypes = [P]
+    L.zd_live_ids.restype = i32
+    L.zd_live_ids.argtypes = [P, P]
+    L.zd_set_stream.restype = i32
+    L.zd_set_stream.argtypes = [P, P]
+    L.zd_free.restype = None
+    L.zd_free.argtypes = [P]
+    L.zd_last_error.restype = C.c_char_p
+    L.zd_last_error.argtypes = []
+    L.zd_last_error_code.restype = i32
+    L.zd_last_error_code.argtypes = []
+    L.zd_get_info.restype = i32
+    L.zd_get_info.argtypes = [P, C.POINTER(_Info)]
+    L.zd_export.restype = i32
+    L.zd_export.argtypes = [P, P, P, P, P, P]
+    L.zd_set_timing.restype = i32
+    L.zd_set_timing.argtypes = [P, i32]
+    L.zd_get_timing.restype = i32
+    L.zd_get_timing.argtypes = [P, C.POINTER(C.c_float), i32]
+    _lib = L
+    return L
+
+
+def last_error() -> str:
+    return load().zd_last_error().decode()
+
+
+def _check(rc: int) -> int:
+    if rc < 0:
+        raise ZdError(rc, last_error())
+    return rc
+
+
+def _ptr(a) -> Optional[int]:
+    """Raw pointer of a contiguous torch tensor / numpy array (None for None)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    if not a.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return a.data_ptr()
+
+
+def _as_i32(a):
+    if isinstance(a, np.ndarray):
+        return np.ascontiguousarray(a, dtype=np.int32)
+    import torch
+    if a.dtype != torch.int32:
+        a = a.to(torch.int32)
+    return a.contiguous()
+
+
+def _current_stream() -> Optional[int]:
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_stream().cuda_stream
+    except Exception:
+        pass
+    return None
+
+
+class ZdTree:
+    """Handle to a device-resident zd-tree (wraps zd_tree*)."""
+
+    def __init__(self, handle: int, dim: int):
+        self._h = handle
+        self.dim = dim
+
+    # -- lifetime
+    def zd_free(self):
+        if self._h:
+            load().zd_free(self._h)
+            self._h = None
+
+    close = zd_free
+
+    def __del__(self):
+        try:
+            self.zd_free()
+        except Exception:
+            pass
+
+    @property
+    def handle(self) -> int:
+        if not self._h:
+            raise ZdError(ZD_EINVAL, "tree already freed")
+        return self._h
+
+    # -- queries
+    def zd_knn(self, k: int, queries=None, out_idx=None, out_dist2=None, device=None):
+        """Exact k-NN.  queries=None: all live points (rows by ascending live id).
+        Returns (out_idx int32 [m,k], out_dist2 int64 [m,k]); allocated on `device`
+        (default: cuda) when not given."""
+        import torch
+        q = None if queries is None else _as_i32(queries)
+        m = self.zd_size() if q is None else int(q.shape[0])
+        if out_idx is None:
+            dev = device or "cuda"
+            out_idx = torch.empty((m, k), dtype=torch.int32, device=dev)
+            out_dist2 = torch.empty((m, k), dtype=torch.int64, device=dev)
+        _check(load().zd_knn(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2)))
+        return out_idx, out_dist2
+
+    def zd_insert(self, batch) -> int:
+        b = _as_i32(batch)
+        return _check(load().zd_insert(self.handle, _ptr(b), int(b.shape[0])))
+
+    def zd_delete(self, ids) -> int:
+        i = _as_i32(ids)
+        return _check(load().zd_delete(self.handle, _ptr(i), int(i.shape[0])))
+
+    def zd_size(self) -> int:
+        return _check(load().zd_size(self.handle))
+
+    def zd_live_ids(self, device=None):
+        import torch
+        out = torch.empty(self.zd_size(), dtype=torch.int32, device=device or "cuda")
+        _check(load().zd_live_ids(self.handle, _ptr(out)))
+        return out
+
+    def zd_set_stream(self, stream) -> None:
+        s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+        _check(load().zd_set_stream(self.handle, s))
+
+    # -- introspection
+    def zd_get_info(self) -> dict:
+        info = _Info()
+        _check(load().zd_get_info(self.handle, C.byref(info)))
+        return {f: getattr(info, f) for f, _ in _Info._fields_}
+
+    def zd_export(self) -> dict:
+        """Host copies of the sorted arrays and the node arrays (numpy)."""
+        info = self.zd_get_info()
+        n, nl, ni, w = info["n"], info["n_leaves"], info["n_internal"], info["node_words"]
+        keys = np.empty(n, np.uint64)
+        recs = np.empty((n, 4), np.int32)
+        ls = np.empty(nl + 1, np.int32)
+        lp = np.empty(nl, np.int32)
+        nodes = np.empty((ni, w), np.int32)
+        _check(load().zd_export(self.handle, _ptr(keys), _ptr(recs), _ptr(ls), _ptr(lp), _ptr(nodes)))
+        return dict(info=info, keys=keys, recs=recs, leaf_start=ls, leaf_parent=lp, nodes=nodes)
+
+    def zd_set_timing(self, enable: bool = True) -> None:
+        _check(load().zd_set_timing(self.handle, int(enable)))
+
+    def zd_get_timing(self) -> dict:
+        buf = (C.c_float * len(PHASES))()
+        c = _check(load().zd_get_timing(self.handle, buf, len(PHASES)))
+        return {PHASES[i]: float(buf[i]) for i in range(c)}
+
+
+def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None, timing: bool = False) -> ZdTree:
+    """Build a zd-tree over int32 points [n, dim] (point i gets id i)."""
+    p = _as_i32(points)
+    n = int(p.shape[0])
+    dim = int(p.shape[1]) if dim is None else dim
+    s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    if s is None:
+        s = _current_stream()
+    opts = _Opts(s, leaf_max, int(timing))
+    h = load().zd_build_ex(_ptr(p) if n else None, n, dim, C.byref(opts))
+    if not h:
+        raise ZdError(load().zd_last_error_code(), last_error())
+    return ZdTree(h, dim)
+
+
+__all__ = ["zd_build", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "PHASES",
+           "ZD_OK", "ZD_EINVAL", "ZD_ERANGE", "ZD_ENOMEM", "ZD_ECUDA"]

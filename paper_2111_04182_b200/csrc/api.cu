@@ -1,0 +1,578 @@
+// api.cu — the C ABI of include/zd.h: handle, device memory, stream, orchestration.
+//
+// Host side only launches kernels (sort.cu, tree.cu, knn.cu, update.cu); every step
+// of the hot path runs on the GPU.  Memory comes from the device's stream-ordered
+// pool (cudaMallocAsync) with the release threshold raised, so repeated builds and
+// updates reuse memory without device-wide synchronisation.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <utility>
+
+#include "../../include/zd.h"
+#include "internal.h"
+
+using namespace zd;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_code = 0;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    g_err_code = code;
+    return code;
+}
+
+void clear_err() {
+    g_err.clear();
+    g_err_code = 0;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    cudaGetLastError();   // clear sticky-free errors
+    const int code = (e == cudaErrorMemoryAllocation) ? ZD_ENOMEM : ZD_ECUDA;
+    return fail(code, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define ZD_CUDA(call)                                              \
+    do {                                                           \
+        cudaError_t e_ = (call);                                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);        \
+    } while (0)
+
+#define ZD_CHECK_LAUNCH(where)                                     \
+    do {                                                           \
+        cudaError_t e_ = cudaGetLastError();                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where);        \
+    } while (0)
+
+void pool_setup_once() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = true;
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count, cudaStream_t st) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    return cudaMallocAsync((void**)p, count * sizeof(T), st);
+}
+
+template <class T>
+void dfree(T*& p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+}
+
+enum Phase { PH_SORT = 0, PH_TOPO = 1, PH_BBOX = 2, PH_MERGE = 3, PH_KNN = 4, PH_VALID = 5, NPH = 6 };
+
+}  // namespace
+
+struct zd_tree {
+    int dim = 3, leaf_max = 16;
+    cudaStream_t st = nullptr;
+    int64_t n = 0, n_next = 0, cap = 0, id_cap = 0;
+    // sorted live points
+    uint64_t* keys = nullptr;
+    int4* recs = nullptr;
+    uint64_t* keys2 = nullptr;
+    int4* recs2 = nullptr;
+    TreeBufs tb{};
+    // id bookkeeping
+    uint32_t* alive = nullptr;     // [id_cap/32] bitset
+    int32_t* row_of_id = nullptr;  // [id_cap]
+    int32_t* live_ids = nullptr;   // [cap]
+    uint32_t* rank_cnt = nullptr;  // [rank_blocks(id_cap)+1]
+    bool rows_identity = true, rows_dirty = false;
+    // small scratch
+    int32_t* d_small = nullptr;    // [0..3] meta copy area, [4] invalid flag, [6..7] u64 count
+    int32_t* h_small = nullptr;    // pinned mirror
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[8] = {};
+    float ms[NPH] = {};
+    bool host_meta_valid = false;
+    int64_t n_leaves = 1, n_internal = 0;
+    int32_t root = ~0;
+};
+
+namespace {
+
+int* d_invalid(zd_tree* h) { return h->d_small + 4; }
+unsigned long long* d_count(zd_tree* h) { return reinterpret_cast<unsigned long long*>(h->d_small + 6); }
+
+void free_tree_bufs(zd_tree* h) {
+    TreeBufs& t = h->tb;
+    dfree(t.pt_leaf, h->st); dfree(t.leaf_start, h->st); dfree(t.leaf_parent, h->st);
+    dfree(t.split_bit, h->st); dfree(t.visit, h->st); dfree(t.range, h->st);
+    dfree(t.flags, h->st); dfree(t.block_cnt, h->st);
+    if (t.nodes) { cudaFreeAsync(t.nodes, h->st); t.nodes = nullptr; }
+}
+
+int alloc_tree_bufs(zd_tree* h, int64_t cap) {
+    free_tree_bufs(h);
+    TreeBufs& t = h->tb;
+    t.d_meta = h->d_small;
+    const size_t node_bytes = h->dim == 2 ? 48 : 64;
+    ZD_CUDA(dalloc(&t.pt_leaf, cap, h->st));
+    ZD_CUDA(dalloc(&t.leaf_start, cap + 2, h->st));
+    ZD_CUDA(dalloc(&t.leaf_parent, cap + 1, h->st));
+    ZD_CUDA(dalloc(&t.split_bit, cap, h->st));
+    ZD_CUDA(dalloc(&t.visit, cap, h->st));
+    ZD_CUDA(dalloc(&t.range, 2 * cap, h->st));
+    ZD_CUDA(dalloc(&t.flags, cap, h->st));
+    ZD_CUDA(dalloc(&t.block_cnt, std::max(tree_blocks(cap), compact_blocks(cap)) + 2, h->st));
+    ZD_CUDA(cudaMallocAsync(&t.nodes, std::max<int64_t>(cap, 1) * node_bytes, h->st));
+    return ZD_OK;
+}
+
+// Point capacity for keys/recs (and their alternates) + tree buffers.
+int ensure_point_cap(zd_tree* h, int64_t need, bool keep_primary) {
+    if (need <= h->cap && h->keys) return ZD_OK;
+    const int64_t cap = std::max<int64_t>(need, h->cap + h->cap / 4);
+    uint64_t* nk = nullptr;
+    int4* nr = nullptr;
+    ZD_CUDA(dalloc(&nk, cap, h->st));
+    ZD_CUDA(dalloc(&nr, cap, h->st));
+    if (keep_primary && h->n > 0) {
+        ZD_CUDA(cudaMemcpyAsync(nk, h->keys, h->n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, h->st));
+        ZD_CUDA(cudaMemcpyAsync(nr, h->recs, h->n * sizeof(int4), cudaMemcpyDeviceToDevice, h->st));
+    }
+    dfree(h->keys, h->st); dfree(h->recs, h->st); dfree(h->keys2, h->st); dfree(h->recs2, h->st);
+    dfree(h->live_ids, h->st);
+    h->keys = nk;
+    h->recs = nr;
+    ZD_CUDA(dalloc(&h->keys2, cap, h->st));
+    ZD_CUDA(dalloc(&h->recs2, cap, h->st));
+    ZD_CUDA(dalloc(&h->live_ids, cap, h->st));
+    h->cap = cap;
+    h->rows_dirty = true;   // live_ids was reallocated
+    return alloc_tree_bufs(h, cap);
+}
+
+int ensure_id_cap(zd_tree* h, int64_t need) {
+    if (need <= h->id_cap && h->alive) return ZD_OK;
+    const int64_t cap = std::max<int64_t>(need, h->id_cap + h->id_cap / 4);
+    const int64_t words = (cap + 31) / 32, old_words = (h->id_cap + 31) / 32;
+    uint32_t* na = nullptr;
+    ZD_CUDA(dalloc(&na, words, h->st));
+    ZD_CUDA(cudaMemsetAsync(na, 0, words * sizeof(uint32_t), h->st));
+    if (h->alive && old_words > 0)
+        ZD_CUDA(cudaMemcpyAsync(na, h->alive, old_words * sizeof(uint32_t), cudaMemcpyDeviceToDevice, h->st));
+    dfree(h->alive, h->st);
+    dfree(h->row_of_id, h->st);
+    dfree(h->rank_cnt, h->st);
+    h->alive = na;
+    ZD_CUDA(dalloc(&h->row_of_id, cap, h->st));
+    ZD_CUDA(dalloc(&h->rank_cnt, rank_blocks(cap) + 2, h->st));
+    h->id_cap = cap;
+    h->rows_dirty = true;
+    return ZD_OK;
+}
+
+// Sorted (keys, recs) of n points with ids id_base.. into the given outputs.
+int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out) {
+    if (n <= 0) return ZD_OK;
+    SortScratch s{};
+    ZD_CUDA(dalloc(&s.k[0], n, h->st));
+    ZD_CUDA(dalloc(&s.k[1], n, h->st));
+    ZD_CUDA(dalloc(&s.v[0], n, h->st));
+    ZD_CUDA(dalloc(&s.v[1], n, h->st));
+    s.zero_words = sort_zero_words(n);
+    ZD_CUDA(dalloc(&s.zero_block, s.zero_words, h->st));
+    ZD_CUDA(dalloc(&s.offs, 8 * 256, h->st));
+    sort_points(h->dim, dpts, n, id_base, keys_out, recs_out, s, d_invalid(h), h->st);
+    ZD_CHECK_LAUNCH("sort_points");
+    dfree(s.k[0], h->st); dfree(s.k[1], h->st); dfree(s.v[0], h->st); dfree(s.v[1], h->st);
+    dfree(s.zero_block, h->st); dfree(s.offs, h->st);
+    return ZD_OK;
+}
+
+void rec(zd_tree* h, int i) {
+    if (h->timing) cudaEventRecord(h->ev[i], h->st);
+}
+
+void elapsed(zd_tree* h, int phase, int a, int b) {
+    float t = 0.f;
+    if (h->timing && cudaEventElapsedTime(&t, h->ev[a], h->ev[b]) == cudaSuccess) h->ms[phase] = t;
+}
+
+int topology(zd_tree* h) {
+    build_topology(h->dim, h->keys, h->recs, h->n, h->leaf_max, h->tb, h->st, h->timing ? h->ev[6] : nullptr);
+    ZD_CHECK_LAUNCH("build_topology");
+    h->host_meta_valid = false;
+    return ZD_OK;
+}
+
+int sync_meta(zd_tree* h) {
+    ZD_CUDA(cudaMemcpyAsync(h->h_small, h->d_small, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+    ZD_CUDA(cudaStreamSynchronize(h->st));
+    return ZD_OK;
+}
+
+int refresh_host_meta(zd_tree* h) {
+    if (h->host_meta_valid) return ZD_OK;
+    int rc = sync_meta(h);
+    if (rc) return rc;
+    h->n_internal = h->h_small[0];
+    h->n_leaves = h->n_internal + 1;
+    h->root = h->h_small[1];
+    h->host_meta_valid = true;
+    return ZD_OK;
+}
+
+int ensure_rows(zd_tree* h) {
+    if (h->rows_identity || !h->rows_dirty) return ZD_OK;
+    rank_alive(h->alive, h->n_next, h->row_of_id, h->live_ids, h->rank_cnt, h->st);
+    ZD_CHECK_LAUNCH("rank_alive");
+    h->rows_dirty = false;
+    return ZD_OK;
+}
+
+// Device copy of a caller array (host or device).  *owned is set when staged.
+int stage_in(zd_tree* h, const void* src, size_t bytes, const void** dev, void** owned) {
+    *owned = nullptr;
+    if (bytes == 0 || is_device_ptr(src)) { *dev = src; return ZD_OK; }
+    void* d = nullptr;
+    ZD_CUDA(cudaMallocAsync(&d, bytes, h->st));
+    ZD_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, h->st));
+    *owned = d;
+    *dev = d;
+    return ZD_OK;
+}
+
+void destroy(zd_tree* h) {
+    if (!h) return;
+    dfree(h->keys, h->st); dfree(h->recs, h->st); dfree(h->keys2, h->st); dfree(h->recs2, h->st);
+    free_tree_bufs(h);
+    dfree(h->alive, h->st); dfree(h->row_of_id, h->st); dfree(h->live_ids, h->st); dfree(h->rank_cnt, h->st);
+    dfree(h->d_small, h->st);
+    cudaStreamSynchronize(h->st);
+    if (h->h_small) cudaFreeHost(h->h_small);
+    for (auto& e : h->ev) if (e) cudaEventDestroy(e);
+    delete h;
+}
+
+int do_build(zd_tree* h, const int32_t* points, int64_t n) {
+    pool_setup_once();
+    ZD_CUDA(dalloc(&h->d_small, 8, h->st));
+    ZD_CUDA(cudaMallocHost((void**)&h->h_small, 8 * sizeof(int32_t)));
+    for (auto& e : h->ev) ZD_CUDA(cudaEventCreate(&e));
+    ZD_CUDA(cudaMemsetAsync(h->d_small, 0, 8 * sizeof(int32_t), h->st));
+    const void* dpts = nullptr;
+    void* owned = nullptr;
+    int rc = stage_in(h, points, (size_t)n * h->dim * sizeof(int32_t), &dpts, &owned);
+    if (rc) return rc;
+    if ((rc = ensure_point_cap(h, std::max<int64_t>(n, 1), false))) return rc;
+    if ((rc = ensure_id_cap(h, std::max<int64_t>(n, 1)))) return rc;
+    h->n = n;
+    h->n_next = n;
+    rec(h, 0);
+    if ((rc = sort_into(h, (const int32_t*)dpts, n, 0, h->keys, h->recs))) return rc;
+    rec(h, 1);
+    if ((rc = topology(h))) return rc;
+    rec(h, 2);
+    set_alive_range(h->alive, 0, n, h->st);
+    h->rows_identity = true;
+    if (owned) cudaFreeAsync(owned, h->st);
+    if ((rc = refresh_host_meta(h))) return rc;   // the one sync: validation flag + node count
+    elapsed(h, PH_SORT, 0, 1);
+    elapsed(h, PH_TOPO, 1, 6);
+    elapsed(h, PH_BBOX, 6, 2);
+    if (h->h_small[4]) return fail(ZD_ERANGE, "zd_build: coordinate outside the universe box [0, 2^B)");
+    return ZD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* zd_last_error(void) { return g_err.c_str(); }
+int zd_last_error_code(void) { return g_err_code; }
+
+zd_tree* zd_build_ex(const int32_t* points, int64_t n, int dim, const zd_opts* opts) {
+    clear_err();
+    if (dim != 2 && dim != 3) { fail(ZD_EINVAL, "zd_build: dim must be 2 or 3"); return nullptr; }
+    if (n < 0 || n >= ((int64_t)1 << 31) - 1) { fail(ZD_EINVAL, "zd_build: need 0 <= n < 2^31-1"); return nullptr; }
+    if (n > 0 && !points) { fail(ZD_EINVAL, "zd_build: points is NULL"); return nullptr; }
+    int leaf_max = 16;
+    cudaStream_t st = nullptr;
+    if (opts) {
+        if (opts->leaf_max) leaf_max = opts->leaf_max;
+        st = (cudaStream_t)opts->stream;
+    }
+    const bool timing = opts && opts->timing;
+    if (leaf_max < 1 || leaf_max > ZD_LEAF_MAX_MAX) { fail(ZD_EINVAL, "zd_build: leaf_max out of range"); return nullptr; }
+    zd_tree* h = new zd_tree();
+    h->dim = dim;
+    h->leaf_max = leaf_max;
+    h->st = st;
+    h->timing = timing;
+    if (do_build(h, points, n) != ZD_OK) {
+        std::string e = g_err;
+        int c = g_err_code;
+        destroy(h);
+        fail(c, e);
+        return nullptr;
+    }
+    return h;
+}
+
+zd_tree* zd_build(const int32_t* points, int64_t n, int dim) { return zd_build_ex(points, n, dim, nullptr); }
+
+void zd_free(zd_tree* h) { destroy(h); }
+
+int64_t zd_size(const zd_tree* h) { return h ? h->n : fail(ZD_EINVAL, "NULL handle"); }
+
+int zd_set_stream(zd_tree* h, void* stream) {
+    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    ZD_CUDA(cudaStreamSynchronize(h->st));
+    h->st = (cudaStream_t)stream;
+    return ZD_OK;
+}
+
+int zd_set_timing(zd_tree* h, int enable) {
+    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    h->timing = enable != 0;
+    return ZD_OK;
+}
+
+int zd_get_timing(const zd_tree* h, float* ms, int nphase) {
+    if (!h || !ms) return fail(ZD_EINVAL, "NULL argument");
+    int c = std::min(nphase, (int)NPH);
+    for (int i = 0; i < c; ++i) ms[i] = h->ms[i];
+    return c;
+}
+
+int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_idx, int64_t* out_dist2) {
+    clear_err();
+    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    if (k < 1 || k > ZD_K_MAX) return fail(ZD_EINVAL, "zd_knn: k must be in [1, ZD_K_MAX]");
+    if (m < 0 || m >= ((int64_t)1 << 31) - 1) return fail(ZD_EINVAL, "zd_knn: bad m");
+    if (!queries && m != h->n) return fail(ZD_EINVAL, "zd_knn: all-points query needs m == zd_size(h)");
+    if (m > 0 && (!out_idx || !out_dist2)) return fail(ZD_EINVAL, "zd_knn: NULL output");
+    if (m == 0) return ZD_OK;
+    int rc;
+    const bool host_out = !is_device_ptr(out_idx) || !is_device_ptr(out_dist2);
+    int32_t* di = out_idx;
+    int64_t* dd = out_dist2;
+    if (host_out) {
+        ZD_CUDA(dalloc(&di, (size_t)m * k, h->st));
+        ZD_CUDA(dalloc(&dd, (size_t)m * k, h->st));
+    }
+    KnnArgs a{};
+    a.dim = h->dim; a.k = k; a.n = h->n;
+    a.recs = h->recs; a.pt_leaf = h->tb.pt_leaf; a.leaf_start = h->tb.leaf_start;
+    a.leaf_parent = h->tb.leaf_parent; a.nodes = h->tb.nodes; a.d_meta = h->d_small;
+    a.out_idx = di; a.out_d2 = dd;
+    if (!queries) {
+        if ((rc = ensure_rows(h))) return rc;
+        a.row_of_id = h->rows_identity ? nullptr : h->row_of_id;
+        rec(h, 0);
+        knn_all(a, h->st);
+        ZD_CHECK_LAUNCH("knn_all");
+        rec(h, 1);
+    } else {
+        const void* dq = nullptr;
+        void* owned = nullptr;
+        if ((rc = stage_in(h, queries, (size_t)m * h->dim * sizeof(int32_t), &dq, &owned))) return rc;
+        ZD_CUDA(cudaMemsetAsync(d_invalid(h), 0, sizeof(int), h->st));
+        validate_points(h->dim, (const int32_t*)dq, m, d_invalid(h), h->st);
+        ZD_CUDA(cudaMemcpyAsync(h->h_small + 4, d_invalid(h), sizeof(int), cudaMemcpyDeviceToHost, h->st));
+        ZD_CUDA(cudaStreamSynchronize(h->st));
+        if (h->h_small[4]) {
+            if (owned) cudaFreeAsync(owned, h->st);
+            if (host_out) { dfree(di, h->st); dfree(dd, h->st); }
+            return fail(ZD_ERANGE, "zd_knn: query outside the universe box");
+        }
+        rec(h, 0);
+        knn_queries(a, (const int32_t*)dq, m, nullptr, h->st);
+        ZD_CHECK_LAUNCH("knn_queries");
+        rec(h, 1);
+        if (owned) cudaFreeAsync(owned, h->st);
+    }
+    if (host_out) {
+        ZD_CUDA(cudaMemcpyAsync(out_idx, di, (size_t)m * k * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+        ZD_CUDA(cudaMemcpyAsync(out_dist2, dd, (size_t)m * k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->st));
+        dfree(di, h->st);
+        dfree(dd, h->st);
+        ZD_CUDA(cudaStreamSynchronize(h->st));
+    }
+    if (h->timing) {
+        ZD_CUDA(cudaEventSynchronize(h->ev[1]));
+        elapsed(h, PH_KNN, 0, 1);
+    }
+    return ZD_OK;
+}
+
+int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
+    clear_err();
+    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    if (m < 0) return fail(ZD_EINVAL, "zd_insert: m < 0");
+    if (m == 0) return h->n_next;
+    if (!batch) return fail(ZD_EINVAL, "zd_insert: batch is NULL");
+    if (h->n_next + m >= ((int64_t)1 << 31) - 1) return fail(ZD_EINVAL, "zd_insert: id space exhausted (2^31)");
+    int rc;
+    const void* db = nullptr;
+    void* owned = nullptr;
+    if ((rc = stage_in(h, batch, (size_t)m * h->dim * sizeof(int32_t), &db, &owned))) return rc;
+    // validation before any mutation
+    rec(h, 0);
+    ZD_CUDA(cudaMemsetAsync(d_invalid(h), 0, sizeof(int), h->st));
+    validate_points(h->dim, (const int32_t*)db, m, d_invalid(h), h->st);
+    ZD_CUDA(cudaMemcpyAsync(h->h_small + 4, d_invalid(h), sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    rec(h, 1);
+    ZD_CUDA(cudaStreamSynchronize(h->st));
+    if (h->h_small[4]) {
+        if (owned) cudaFreeAsync(owned, h->st);
+        return fail(ZD_ERANGE, "zd_insert: coordinate outside the universe box (tree unchanged)");
+    }
+    const int64_t first = h->n_next;
+    // sorted batch with ids first.. (K7)
+    uint64_t* bk = nullptr;
+    int4* br = nullptr;
+    ZD_CUDA(dalloc(&bk, m, h->st));
+    ZD_CUDA(dalloc(&br, m, h->st));
+    rec(h, 2);
+    if ((rc = sort_into(h, (const int32_t*)db, m, (uint32_t)first, bk, br))) return rc;
+    if (owned) cudaFreeAsync(owned, h->st);
+    rec(h, 3);
+    if ((rc = ensure_point_cap(h, h->n + m, true))) return rc;
+    if ((rc = ensure_id_cap(h, first + m))) return rc;
+    // merge into the alternate buffers (K8), then swap
+    merge_sorted(h->keys, h->recs, h->n, bk, br, m, h->keys2, h->recs2, h->st);
+    ZD_CHECK_LAUNCH("merge_sorted");
+    std::swap(h->keys, h->keys2);
+    std::swap(h->recs, h->recs2);
+    dfree(bk, h->st);
+    dfree(br, h->st);
+    set_alive_range(h->alive, first, m, h->st);
+    h->n += m;
+    h->n_next += m;
+    if (!h->rows_identity) h->rows_dirty = true;
+    rec(h, 4);
+    if ((rc = topology(h))) return rc;
+    rec(h, 5);
+    if (h->timing) {
+        ZD_CUDA(cudaEventSynchronize(h->ev[5]));
+        elapsed(h, PH_VALID, 0, 1);
+        elapsed(h, PH_SORT, 2, 3);
+        elapsed(h, PH_MERGE, 3, 4);
+        elapsed(h, PH_TOPO, 4, 6);
+        elapsed(h, PH_BBOX, 6, 5);
+    }
+    return first;
+}
+
+int64_t zd_delete(zd_tree* h, const int32_t* ids, int64_t m) {
+    clear_err();
+    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    if (m < 0) return fail(ZD_EINVAL, "zd_delete: m < 0");
+    if (m == 0 || h->n == 0) return 0;
+    if (!ids) return fail(ZD_EINVAL, "zd_delete: ids is NULL");
+    int rc;
+    const void* di = nullptr;
+    void* owned = nullptr;
+    if ((rc = stage_in(h, ids, (size_t)m * sizeof(int32_t), &di, &owned))) return rc;
+    rec(h, 0);
+    ZD_CUDA(cudaMemsetAsync(d_count(h), 0, sizeof(unsigned long long), h->st));
+    mark_deleted(h->alive, h->n_next, (const int32_t*)di, m, d_count(h), h->st);
+    compact_alive(h->alive, h->keys, h->recs, h->n, h->keys2, h->recs2, h->tb.block_cnt, h->st);
+    ZD_CHECK_LAUNCH("delete");
+    if (owned) cudaFreeAsync(owned, h->st);
+    ZD_CUDA(cudaMemcpyAsync(h->h_small + 6, d_count(h), sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+    rec(h, 1);
+    ZD_CUDA(cudaStreamSynchronize(h->st));
+    unsigned long long cnt;
+    std::memcpy(&cnt, h->h_small + 6, sizeof(cnt));
+    if (cnt == 0) return 0;
+    std::swap(h->keys, h->keys2);
+    std::swap(h->recs, h->recs2);
+    h->n -= (int64_t)cnt;
+    h->rows_identity = false;
+    h->rows_dirty = true;
+    rec(h, 2);
+    if ((rc = topology(h))) return rc;
+    rec(h, 3);
+    if (h->timing) {
+        ZD_CUDA(cudaEventSynchronize(h->ev[3]));
+        elapsed(h, PH_MERGE, 0, 1);
+        elapsed(h, PH_TOPO, 2, 6);
+        elapsed(h, PH_BBOX, 6, 3);
+    }
+    return (int64_t)cnt;
+}
+
+int zd_live_ids(const zd_tree* hc, int32_t* out) {
+    clear_err();
+    zd_tree* h = const_cast<zd_tree*>(hc);
+    if (!h || (!out && h->n > 0)) return fail(ZD_EINVAL, "NULL argument");
+    if (h->n == 0) return ZD_OK;
+    int rc;
+    if (h->rows_identity) {
+        // ids 0..n-1 are all alive: identity
+        rank_alive(h->alive, h->n_next, h->row_of_id, h->live_ids, h->rank_cnt, h->st);
+        ZD_CHECK_LAUNCH("rank_alive");
+    } else if ((rc = ensure_rows(h))) {
+        return rc;
+    }
+    ZD_CUDA(cudaMemcpyAsync(out, h->live_ids, h->n * sizeof(int32_t), cudaMemcpyDefault, h->st));
+    ZD_CUDA(cudaStreamSynchronize(h->st));
+    return ZD_OK;
+}
+
+int zd_get_info(const zd_tree* hc, zd_info* out) {
+    zd_tree* h = const_cast<zd_tree*>(hc);
+    if (!h || !out) return fail(ZD_EINVAL, "NULL argument");
+    int rc = refresh_host_meta(h);
+    if (rc) return rc;
+    out->dim = h->dim;
+    out->leaf_max = h->leaf_max;
+    out->n = h->n;
+    out->n_next = h->n_next;
+    out->n_leaves = h->n_leaves;
+    out->n_internal = h->n_internal;
+    out->root = h->root;
+    out->node_words = h->dim == 2 ? 12 : 16;
+    return ZD_OK;
+}
+
+int zd_export(const zd_tree* hc, uint64_t* keys, int32_t* recs, int32_t* leaf_start, int32_t* leaf_parent,
+              int32_t* nodes) {
+    zd_tree* h = const_cast<zd_tree*>(hc);
+    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    int rc = refresh_host_meta(h);
+    if (rc) return rc;
+    const cudaMemcpyKind K = cudaMemcpyDefault;
+    if (keys && h->n) ZD_CUDA(cudaMemcpyAsync(keys, h->keys, h->n * sizeof(uint64_t), K, h->st));
+    if (recs && h->n) ZD_CUDA(cudaMemcpyAsync(recs, h->recs, h->n * sizeof(int4), K, h->st));
+    if (leaf_start) ZD_CUDA(cudaMemcpyAsync(leaf_start, h->tb.leaf_start, (h->n_leaves + 1) * sizeof(int32_t), K, h->st));
+    if (leaf_parent) ZD_CUDA(cudaMemcpyAsync(leaf_parent, h->tb.leaf_parent, h->n_leaves * sizeof(int32_t), K, h->st));
+    if (nodes && h->n_internal)
+        ZD_CUDA(cudaMemcpyAsync(nodes, h->tb.nodes, h->n_internal * (h->dim == 2 ? 48 : 64), K, h->st));
+    ZD_CUDA(cudaStreamSynchronize(h->st));
+    return ZD_OK;
+}
+
+}  // extern "C"

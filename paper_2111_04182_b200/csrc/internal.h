@@ -1,0 +1,83 @@
+// internal.h — host-side launch interface between the CUDA translation units.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace zd {
+
+// ---------------------------------------------------------------- sort (sort.cu)
+// One-sweep LSD radix sort of (Morton key, id): 8 passes x 8-bit digits, one
+// up-front histogram of all 8 digits, decoupled look-back per pass.
+struct SortScratch {
+    uint64_t* k[2];        // ping-pong keys   [cap]
+    uint32_t* v[2];        // ping-pong ids    [cap]
+    uint32_t* zero_block;  // hist[8*256] | counters[8] | status[8*tiles*256] (memset as one block)
+    uint32_t* offs;        // [8*256] exclusive digit offsets
+    size_t zero_words;
+};
+size_t sort_tiles(int64_t n);
+size_t sort_zero_words(int64_t n);
+// Encode pts (int32 [n][dim]) and sort; ids = id_base + i.  Writes sorted keys
+// and records int4(x, y, z|0, id).  Sets *d_invalid != 0 if a coordinate is out of
+// the universe box.
+void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out,
+                 int4* recs_out, const SortScratch& s, int* d_invalid, cudaStream_t st);
+
+// ---------------------------------------------------------------- tree (tree.cu)
+struct TreeBufs {
+    int32_t* pt_leaf;      // [cap]   leaf of each sorted position
+    int32_t* leaf_start;   // [cap+2]
+    int32_t* leaf_parent;  // [cap+1]
+    int32_t* split_bit;    // [cap]   per internal node (in-order)
+    void* nodes;           // [cap]   Node<dim>
+    uint32_t* visit;       // [cap]   bottom-up arrival counters
+    int32_t* range;        // [2*cap] bottom-up leaf-range scratch
+    uint8_t* flags;        // [cap]   big-pair flags
+    uint32_t* block_cnt;   // [tree_blocks(cap)+1]
+    int32_t* d_meta;       // [4]: nb (internal count), root ref
+};
+size_t tree_blocks(int64_t n);
+// Canonical topology (K4) + bottom-up boxes (K5) over sorted keys/records.
+void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, int leaf_max,
+                    const TreeBufs& t, cudaStream_t st, cudaEvent_t ev_mid);
+
+// ---------------------------------------------------------------- knn (knn.cu)
+struct KnnArgs {
+    int dim, k;
+    int64_t n;                   // live points
+    const int4* recs;
+    const int32_t* pt_leaf;
+    const int32_t* leaf_start;
+    const int32_t* leaf_parent;
+    const void* nodes;
+    const int32_t* d_meta;       // root ref at [1]
+    const int32_t* row_of_id;    // NULL: row = id
+    int32_t* out_idx;
+    int64_t* out_d2;
+};
+int knn_kmax();
+void knn_all(const KnnArgs& a, cudaStream_t st);
+// External queries: pts int32 [m][dim] (validated), bit-based leaf location.
+void knn_queries(const KnnArgs& a, const int32_t* queries, int64_t m, int* d_invalid, cudaStream_t st);
+
+// ---------------------------------------------------------------- updates (update.cu)
+void validate_points(int dim, const int32_t* pts, int64_t m, int* d_invalid, cudaStream_t st);
+// Merge sorted (ka, ra)[n] with sorted (kb, rb)[m] by key (a before b on equal keys).
+void merge_sorted(const uint64_t* ka, const int4* ra, int64_t n, const uint64_t* kb, const int4* rb,
+                  int64_t m, uint64_t* ko, int4* ro, cudaStream_t st);
+// alive bitset ops
+void set_alive_range(uint32_t* alive, int64_t first, int64_t count, cudaStream_t st);
+void mark_deleted(uint32_t* alive, int64_t id_cap, const int32_t* ids, int64_t m,
+                  unsigned long long* d_count, cudaStream_t st);
+// keep sorted positions whose id is alive; returns nothing (count known from d_count)
+void compact_alive(const uint32_t* alive, const uint64_t* ki, const int4* ri, int64_t n,
+                   uint64_t* ko, int4* ro, uint32_t* block_cnt, cudaStream_t st);
+size_t compact_blocks(int64_t n);
+// row_of_id[id] = rank of id among alive ids (for ids < id_cap); live_ids[rank] = id
+void rank_alive(const uint32_t* alive, int64_t id_cap, int32_t* row_of_id, int32_t* live_ids,
+                uint32_t* block_cnt, cudaStream_t st);
+size_t rank_blocks(int64_t id_cap);
+
+}  // namespace zd

@@ -1,0 +1,237 @@
+// sort.cu — K1 Morton encode + K2 one-sweep LSD radix sort of (key, id) + K3 records.
+//
+// PAPER.md P:235 (§2 "Construction": "We then sort the points by the Morton
+// order"), P:416 (Thm 2.1: "a parallel radix sort can be used").
+// B200 design (not the paper's): 8 passes of 8-bit digits over 64-bit keys; one
+// up-front histogram kernel computes all 8 digit histograms while encoding (and
+// range-checking) the points; each pass is ONE kernel that ranks a 3840-key tile
+// with warp-level match, publishes its per-digit counts, resolves its global
+// offsets by decoupled look-back over predecessor tiles (dynamic tile ids, so
+// every predecessor is resident or done), stages the tile in shared memory in
+// digit order and scatters runs of equal digits coalesced.  Pass 1 reads the
+// int32 points directly (encode fused, ids = iota); the last pass decodes the
+// coordinates from the key and writes the 16-byte records (K3 fused).
+#include <cuda/atomic>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace zd {
+
+namespace {
+
+constexpr int ST = 256;              // threads per tile
+constexpr int SI = 15;               // keys per thread
+constexpr int STILE = ST * SI;       // 3840 keys per tile
+constexpr int SW = ST / 32;          // warps
+constexpr int WITEMS = 32 * SI;      // contiguous keys per warp
+constexpr int NPASS = 8;
+constexpr uint32_t VAL_MASK = (1u << 30) - 1;
+constexpr uint32_t FLAG_AGG = 1u << 30;
+constexpr uint32_t FLAG_INC = 2u << 30;
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+    return cuda::atomic_ref<const uint32_t, cuda::thread_scope_device>(*p).load(cuda::memory_order_relaxed);
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+    cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(*p).store(v, cuda::memory_order_relaxed);
+}
+
+template <int DIM>
+__device__ __forceinline__ uint64_t load_key_from_points(const int32_t* __restrict__ pts, uint32_t i, bool& bad) {
+    const int32_t* p = pts + (size_t)i * DIM;
+    int x = __ldg(p), y = __ldg(p + 1), z = DIM == 3 ? __ldg(p + 2) : 0;
+    bad |= !in_universe<DIM>(x, y, z);
+    return morton<DIM>(x, y, z);
+}
+
+// Up-front histogram of all 8 digits (+ range validation).
+template <int DIM>
+__global__ void __launch_bounds__(256) hist_kernel(const int32_t* __restrict__ pts, uint32_t n,
+                                                   uint32_t* __restrict__ g_hist, int* __restrict__ invalid) {
+    __shared__ uint32_t sh[NPASS][256];
+    for (int i = threadIdx.x; i < NPASS * 256; i += 256) (&sh[0][0])[i] = 0;
+    __syncthreads();
+    bool bad = false;
+    for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
+        uint64_t key = load_key_from_points<DIM>(pts, i, bad);
+#pragma unroll
+        for (int p = 0; p < NPASS; ++p) atomicAdd(&sh[p][(key >> (8 * p)) & 255], 1u);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(invalid, 1);
+    for (int i = threadIdx.x; i < NPASS * 256; i += 256) {
+        uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(g_hist + i, v);
+    }
+}
+
+__global__ void __launch_bounds__(256) scan_hist_kernel(const uint32_t* __restrict__ g_hist, uint32_t* __restrict__ offs) {
+    __shared__ uint32_t s_warp[32];
+    for (int p = 0; p < NPASS; ++p) {
+        uint32_t v = g_hist[p * 256 + threadIdx.x];
+        offs[p * 256 + threadIdx.x] = block_exclusive_scan<256>(v, s_warp, nullptr);
+    }
+}
+
+// MODE 0: first pass (encode points), 1: middle pass, 2: last pass (write records).
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(ST) onesweep_kernel(
+    const int32_t* __restrict__ pts, const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ ids_in,
+    uint64_t* __restrict__ keys_out, uint32_t* __restrict__ ids_out, int4* __restrict__ recs_out,
+    uint32_t n, int shift, uint32_t id_base, const uint32_t* __restrict__ digit_offs,
+    uint32_t* status, uint32_t* tile_counter) {
+    __shared__ union {
+        uint32_t hist[SW][256];
+        uint64_t keys[STILE];
+    } u;
+    __shared__ uint32_t s_ids[STILE];
+    __shared__ uint32_t s_start[256];
+    __shared__ uint32_t s_glob[256];
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_tile;
+
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
+    for (int i = tid; i < SW * 256; i += ST) (&u.hist[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint32_t tile_base = tile * STILE;
+    const uint32_t base = tile_base + w * WITEMS + lane;
+
+    // ---- load (warp-blocked: warp w owns 480 contiguous keys, so rank order = input order)
+    uint64_t key[SI];
+    uint32_t id[SI];
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < SI; ++j) {
+        uint32_t idx = base + j * 32;
+        if (idx < n) {
+            if (MODE == 0) {
+                key[j] = load_key_from_points<DIM>(pts, idx, bad);
+                id[j] = id_base + idx;
+            } else {
+                key[j] = keys_in[idx];
+                id[j] = ids_in[idx];
+            }
+        } else {
+            key[j] = ~0ull;   // sorts last within the tile; never written out
+            id[j] = 0;
+        }
+    }
+
+    // ---- warp-level ranking: peers with the same digit via match.any
+    uint32_t loc[SI];
+    const uint32_t lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < SI; ++j) {
+        uint32_t d = (uint32_t)(key[j] >> shift) & 255u;
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t lower = __popc(peers & lt_mask);
+        uint32_t old = u.hist[w][d];
+        __syncwarp();
+        if (lower == 0) u.hist[w][d] = old + __popc(peers);
+        __syncwarp();
+        loc[j] = old + lower;
+    }
+    __syncthreads();
+
+    // ---- per-digit tile counts (thread = digit) and warp prefixes
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int ww = 0; ww < SW; ++ww) {
+        uint32_t c = u.hist[ww][tid];
+        u.hist[ww][tid] = cnt;
+        cnt += c;
+    }
+    uint32_t* my_status = status + (size_t)tile * 256 + tid;
+    if (tile == 0) st_relaxed(my_status, FLAG_INC | cnt);
+    else st_relaxed(my_status, FLAG_AGG | cnt);
+
+    const uint32_t start = block_exclusive_scan<ST>(cnt, s_warp, nullptr);
+    s_start[tid] = start;
+
+    // ---- decoupled look-back (one digit per thread)
+    uint32_t excl = 0;
+    if (tile > 0) {
+        const uint32_t* p = status + (size_t)(tile - 1) * 256 + tid;
+        while (true) {
+            uint32_t v = ld_relaxed(p);
+            if ((v & ~VAL_MASK) == 0) continue;   // predecessor not published yet
+            excl += v & VAL_MASK;
+            if ((v & ~VAL_MASK) == FLAG_INC) break;
+            p -= 256;
+        }
+        st_relaxed(my_status, FLAG_INC | (excl + cnt));
+    }
+    s_glob[tid] = digit_offs[tid] + excl - start;
+    __syncthreads();
+
+#pragma unroll
+    for (int j = 0; j < SI; ++j) {
+        uint32_t d = (uint32_t)(key[j] >> shift) & 255u;
+        loc[j] += s_start[d] + u.hist[w][d];
+    }
+    __syncthreads();   // all hist reads done before the union is reused for keys
+#pragma unroll
+    for (int j = 0; j < SI; ++j) {
+        u.keys[loc[j]] = key[j];
+        s_ids[loc[j]] = id[j];
+    }
+    __syncthreads();
+
+    // ---- scatter in digit order: runs of equal digits go to consecutive addresses
+    const uint32_t valid = min((uint32_t)STILE, n - tile_base);
+    for (uint32_t i = tid; i < valid; i += ST) {
+        uint64_t k = u.keys[i];
+        uint32_t d = (uint32_t)(k >> shift) & 255u;
+        uint32_t dest = s_glob[d] + i;
+        keys_out[dest] = k;
+        if (MODE == 2) recs_out[dest] = decode_rec<DIM>(k, (int)s_ids[i]);
+        else ids_out[dest] = s_ids[i];
+    }
+    (void)bad;
+}
+
+template <int DIM>
+void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
+                   const SortScratch& s, int* d_invalid, cudaStream_t st) {
+    const uint32_t un = (uint32_t)n;
+    const size_t tiles = sort_tiles(n);
+    uint32_t* hist = s.zero_block;
+    uint32_t* counters = hist + NPASS * 256;
+    uint32_t* status = counters + NPASS;
+    cudaMemsetAsync(s.zero_block, 0, sort_zero_words(n) * sizeof(uint32_t), st);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int hb = (int)std::min<size_t>((size_t)sms * 8, (n + 255) / 256);
+    hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid);
+    scan_hist_kernel<<<1, 256, 0, st>>>(hist, s.offs);
+    for (int p = 0; p < NPASS; ++p) {
+        uint32_t* stp = status + (size_t)p * tiles * 256;
+        const uint32_t* off = s.offs + p * 256;
+        if (p == 0)
+            onesweep_kernel<DIM, 0><<<tiles, ST, 0, st>>>(pts, nullptr, nullptr, s.k[0], s.v[0], nullptr, un, 0,
+                                                          id_base, off, stp, counters + p);
+        else if (p < NPASS - 1)
+            onesweep_kernel<DIM, 1><<<tiles, ST, 0, st>>>(nullptr, s.k[(p - 1) & 1], s.v[(p - 1) & 1], s.k[p & 1],
+                                                          s.v[p & 1], nullptr, un, 8 * p, 0, off, stp, counters + p);
+        else
+            onesweep_kernel<DIM, 2><<<tiles, ST, 0, st>>>(nullptr, s.k[(p - 1) & 1], s.v[(p - 1) & 1], keys_out,
+                                                          nullptr, recs_out, un, 8 * p, 0, off, stp, counters + p);
+    }
+}
+
+}  // namespace
+
+size_t sort_tiles(int64_t n) { return (size_t)((n + STILE - 1) / STILE); }
+size_t sort_zero_words(int64_t n) { return NPASS * 256 + NPASS + (size_t)NPASS * sort_tiles(n) * 256; }
+
+void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
+                 const SortScratch& s, int* d_invalid, cudaStream_t st) {
+    if (n <= 0) return;
+    if (dim == 2) sort_points_t<2>(pts, n, id_base, keys_out, recs_out, s, d_invalid, st);
+    else sort_points_t<3>(pts, n, id_base, keys_out, recs_out, s, d_invalid, st);
+}
+
+}  // namespace zd

@@ -1,0 +1,203 @@
+// tree.cu — K4 canonical topology + K5 bottom-up bounding boxes.
+//
+// The tree is Alg. 1 buildTree with empty cuts skipped
+// (P:463): node = sorted range [lo, hi); leaf iff hi-lo <= leaf_max or all keys
+// equal; otherwise cut at b = msb(key[lo] ^ key[hi-1]) and split at the first index
+// whose bit b is 1 (splitUsingBit).  Boxes are the tight per-axis bounds of a
+// node's points ("two opposing corners"; SURVEY reading 7).
+//
+// Flat data-parallel construction (not the paper's fork-join recursion):
+//  * delta_p = msb(key_p ^ key_{p+1}) for adjacent sorted keys (-1 if equal).  The
+//    full radix tree is the Cartesian tree of delta: the node whose cut is at pair p
+//    spans [L+1, R+1) where L / R are the nearest pairs left / right of p with a
+//    larger delta.  That node holds more than leaf_max points and has distinct
+//    keys ("big") iff delta_p >= 0 and R - L > leaf_max, which a thread decides by
+//    looking at most leaf_max-1 pairs to each side (shared-memory window).
+//  * Collapsing every small subtree into a leaf leaves exactly the big pairs as
+//    internal nodes; the leaves are the gaps between consecutive big pairs, and the
+//    internal nodes form the Cartesian tree of the big pairs' deltas (nearest larger
+//    neighbours are ancestors, hence big).  A scan over the flags numbers internal
+//    nodes in-order: internal node i separates leaf i from leaf i+1.
+//  * One thread per leaf computes the leaf box and climbs: the parent of a node
+//    spanning leaves [Ll, Rl] is the boundary pair with the smaller delta (the two
+//    boundary deltas always differ).  The first child to arrive at a parent stops;
+//    the second merges both boxes and continues (atomic arrival counter).  Linear
+//    work, one pass, no recursion.
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace zd {
+
+namespace {
+
+constexpr int TT = 256;
+constexpr int TPI = 4;
+constexpr int TTILE = TT * TPI;   // pairs per block
+constexpr int HALO = kMaxLeaf;
+
+__device__ __forceinline__ int delta_of(uint64_t a, uint64_t b) {
+    uint64_t x = a ^ b;
+    return x ? 63 - __clzll((long long)x) : -1;
+}
+
+__global__ void __launch_bounds__(TT) flags_kernel(const uint64_t* __restrict__ keys, uint32_t n, int leaf_max,
+                                                   uint8_t* __restrict__ flags, uint32_t* __restrict__ block_cnt) {
+    __shared__ int8_t s_delta[TTILE + 2 * HALO];
+    __shared__ uint32_t s_warp[32];
+    const int64_t base = (int64_t)blockIdx.x * TTILE;
+    const int64_t npairs = (int64_t)n - 1;
+    for (int t = threadIdx.x; t < TTILE + 2 * HALO; t += TT) {
+        int64_t p = base - HALO + t;
+        // out-of-range pairs act as +infinity: the range boundary
+        s_delta[t] = (p >= 0 && p < npairs) ? (int8_t)delta_of(keys[p], keys[p + 1]) : (int8_t)127;
+    }
+    __syncthreads();
+    const int W = leaf_max - 1;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < TPI; ++i) {
+        const int off = threadIdx.x + i * TT;
+        const int64_t p = base + off;
+        if (p >= npairs) continue;
+        const int c = HALO + off;
+        const int d = s_delta[c];
+        bool big = false;
+        if (d >= 0) {
+            int l = 1, r = 1;
+            while (l <= W && s_delta[c - l] <= d) ++l;
+            while (r <= W && s_delta[c + r] <= d) ++r;
+            big = (l + r) > leaf_max;   // node size = l + r
+        }
+        flags[p] = big;
+        cnt += big;
+    }
+    uint32_t total;
+    block_exclusive_scan<TT>(cnt, s_warp, &total);
+    if (threadIdx.x == 0) block_cnt[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(TT) compact_kernel(const uint8_t* __restrict__ flags, const uint64_t* __restrict__ keys,
+                                                     uint32_t n, const uint32_t* __restrict__ block_off,
+                                                     int32_t* __restrict__ split_bit, int32_t* __restrict__ leaf_start,
+                                                     int32_t* __restrict__ pt_leaf, int32_t* __restrict__ meta,
+                                                     uint32_t* __restrict__ visit) {
+    __shared__ uint32_t s_warp[32];
+    const int64_t base = (int64_t)blockIdx.x * TTILE + threadIdx.x * TPI;   // blocked per thread
+    const int64_t npairs = (int64_t)n - 1;
+    uint8_t f[TPI];
+    uint32_t c = 0;
+#pragma unroll
+    for (int i = 0; i < TPI; ++i) {
+        int64_t p = base + i;
+        f[i] = p < npairs ? flags[p] : 0;
+        c += f[i];
+    }
+    uint32_t run = block_off[blockIdx.x] + block_exclusive_scan<TT>(c, s_warp, nullptr);
+#pragma unroll
+    for (int i = 0; i < TPI; ++i) {
+        int64_t p = base + i;
+        if (p < n) pt_leaf[p] = (int32_t)run;   // leaf = number of big pairs before p
+        if (f[i]) {
+            split_bit[run] = delta_of(keys[p], keys[p + 1]);
+            leaf_start[run + 1] = (int32_t)(p + 1);
+            visit[run] = 0u;   // bottom-up arrival counter of internal node `run`
+            ++run;
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        uint32_t nb = block_off[gridDim.x];
+        meta[0] = (int32_t)nb;
+        meta[1] = nb == 0 ? ~0 : -1;   // root: single leaf, or set by the bottom-up pass
+        leaf_start[0] = 0;
+        leaf_start[nb + 1] = (int32_t)n;
+    }
+}
+
+template <int DIM>
+__device__ __forceinline__ void store_box(int32_t* dst, const int32_t (&b)[2 * DIM]) {
+#pragma unroll
+    for (int a = 0; a < 2 * DIM; ++a) dst[a] = b[a];
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__ recs, const int32_t* __restrict__ leaf_start,
+                                                        const int32_t* __restrict__ split_bit, int32_t* meta,
+                                                        Node<DIM>* nodes, int32_t* __restrict__ leaf_parent,
+                                                        uint32_t* visit, int32_t* range) {
+    const int32_t nb = meta[0];
+    for (int32_t l = blockIdx.x * blockDim.x + threadIdx.x; l <= nb; l += gridDim.x * blockDim.x) {
+        // leaf box from its records
+        int32_t bb[2 * DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) { bb[a] = INT32_MAX; bb[DIM + a] = INT32_MIN; }
+        const int32_t s = leaf_start[l], e = leaf_start[l + 1];
+        for (int32_t j = s; j < e; ++j) {
+            int4 r = __ldg(recs + j);
+            int c[3] = {r.x, r.y, r.z};
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) { bb[a] = min(bb[a], c[a]); bb[DIM + a] = max(bb[DIM + a], c[a]); }
+        }
+        if (nb == 0) { leaf_parent[0] = -1; continue; }
+        int32_t L = l, R = l, ref = ~l;
+        while (true) {
+            bool as_right;
+            int32_t par;
+            if (L == 0) { par = R; as_right = false; }
+            else if (R == nb) { par = L - 1; as_right = true; }
+            else if (__ldg(split_bit + L - 1) < __ldg(split_bit + R)) { par = L - 1; as_right = true; }
+            else { par = R; as_right = false; }
+            Node<DIM>* P = nodes + par;
+            if (as_right) { store_box<DIM>(P->rbox, bb); P->right = ref; range[2 * par + 1] = R; }
+            else { store_box<DIM>(P->lbox, bb); P->left = ref; range[2 * par] = L; }
+            if (ref < 0) leaf_parent[~ref] = par; else nodes[ref].parent = par;
+            __threadfence();
+            if (atomicAdd(visit + par, 1u) == 0) break;   // first child: the sibling finishes the parent
+            __threadfence();
+            const int32_t* sb = as_right ? P->lbox : P->rbox;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a) {
+                bb[a] = min(bb[a], __ldcg(sb + a));
+                bb[DIM + a] = max(bb[DIM + a], __ldcg(sb + DIM + a));
+            }
+            if (as_right) L = __ldcg(range + 2 * par); else R = __ldcg(range + 2 * par + 1);
+            P->split = __ldg(split_bit + par);
+            ref = par;
+            if (L == 0 && R == nb) { P->parent = -1; meta[1] = par; break; }
+        }
+    }
+}
+
+}  // namespace
+
+size_t tree_blocks(int64_t n) { return (size_t)std::max<int64_t>(1, (n - 1 + TTILE - 1) / TTILE); }
+
+void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, int leaf_max, const TreeBufs& t,
+                    cudaStream_t st, cudaEvent_t ev_mid) {
+    const uint32_t un = (uint32_t)n;
+    const size_t nblk = tree_blocks(n);
+    if (n <= 1) {
+        // 0 or 1 point: a single (possibly empty) leaf; reuse the compaction kernel's
+        // bookkeeping path with an empty pair range.
+        cudaMemsetAsync(t.block_cnt, 0, 2 * sizeof(uint32_t), st);
+        compact_kernel<<<1, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta, t.visit);
+    } else {
+        flags_kernel<<<nblk, TT, 0, st>>>(keys, un, leaf_max, t.flags, t.block_cnt);
+        scan_blocks_kernel<<<1, 1024, 0, st>>>(t.block_cnt, (uint32_t)nblk);
+        compact_kernel<<<nblk, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta, t.visit);
+    }
+    if (ev_mid) cudaEventRecord(ev_mid, st);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int grid = (int)std::min<int64_t>((int64_t)sms * 16, std::max<int64_t>(1, (n / 8 + 127) / 128));
+    if (dim == 2)
+        bottom_up_kernel<2><<<grid, 128, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<2>*)t.nodes,
+                                                  t.leaf_parent, t.visit, t.range);
+    else
+        bottom_up_kernel<3><<<grid, 128, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<3>*)t.nodes,
+                                                  t.leaf_parent, t.visit, t.range);
+}
+
+}  // namespace zd

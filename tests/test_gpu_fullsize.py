@@ -1,0 +1,53 @@
+"""Full-size parity on the five BASELINE.json configs, in the launch configuration
+bench.py times (same zd_build / zd_insert / zd_delete / zd_knn calls, k = 10).
+
+Every row of the GPU output is compared bit-exactly with the oracle's leaf-based
+search (itself pinned to brute force in test_oracle_pins.py), and 1,000 seeded
+sample rows per config are also compared with plain brute force over all points.
+"""
+import numpy as np
+import pytest
+import torch
+
+import zdgen
+from parity_util import first_row_mismatch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+K = 10
+
+
+def _run(zd, oracle_mod, name):
+    c = zdgen.CONFIGS[name]
+    pts = zdgen.config_points(name)
+    t = zd.zd_build(torch.from_numpy(pts).cuda())
+    live = oracle_mod.LiveSet(pts)
+    if "insert_m" in c:
+        b = zdgen.insert_batch(c["insert_m"], c["dim"], c["insert_seed"])
+        assert t.zd_insert(torch.from_numpy(b).cuda()) == live.insert(b)
+        kill = zdgen.delete_ids(c["n"], c["delete_m"], c["delete_seed"])
+        assert t.zd_delete(torch.from_numpy(kill).cuda()) == live.delete(kill) == c["delete_m"]
+    gi, gd = t.zd_knn(K)
+    torch.cuda.synchronize()
+    gi, gd = gi.cpu().numpy(), gd.cpu().numpy()
+    ot = live.tree()
+    oi, od, cnt = ot.knn_all(K)
+    bad = first_row_mismatch(gi, gd, oi, od)
+    assert bad.size == 0, f"{name}: {bad.size} rows differ (first {bad[:5]})"
+    # 1,000 sampled rows vs plain brute force over all live points
+    ids = live.live_ids()
+    rng = np.random.default_rng(1234)
+    rows = np.sort(rng.choice(len(ids), size=min(1000, len(ids)), replace=False))
+    order = np.argsort(live.ids)
+    P, I = live.points[order], live.ids[order]              # ascending id = row order
+    bi, bd = oracle_mod.brute_knn(P, I, P[rows], I[rows], K)
+    assert np.array_equal(gi[rows], bi) and np.array_equal(gd[rows], bd)
+    assert np.array_equal(t.zd_live_ids().cpu().numpy(), ids)
+    info = t.zd_get_info()
+    assert info["n_internal"] == (ot.nodes()["split"] >= 0).sum()
+    return info, cnt
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4a", "C4b", "C5"])
+def test_config_full(zd, oracle_mod, name):
+    _run(zd, oracle_mod, name)

@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Sizes span several sort tiles (3840 keys), several topology blocks (1024 pairs) and
+ragged tails; edge cases cover empty / single / duplicate-heavy inputs, every k
+template and leaf sizes 1..32.
+"""
+import numpy as np
+import pytest
+import torch
+
+import zdgen
+from parity_util import assert_same_structure, first_row_mismatch
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_knn_all(tree, k):
+    oi, od = tree.zd_knn(k)
+    torch.cuda.synchronize()
+    return oi.cpu().numpy(), od.cpu().numpy()
+
+
+def check_rows(gi, gd, oi, od):
+    bad = first_row_mismatch(gi, gd, oi, od)
+    assert bad.size == 0, f"{bad.size} rows differ, first row {bad[0]}: gpu {gi[bad[0]]} {gd[bad[0]]} oracle {oi[bad[0]]} {od[bad[0]]}"
+
+
+SIZES = [0, 1, 2, 3, 16, 17, 33, 1000, 3839, 3840, 3841, 20011]
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("dim", [2, 3])
+def test_sort_and_structure_sizes(zd, oracle_mod, n, dim):
+    pts = zdgen.uniform(n, dim, seed=100 + n)
+    t = zd.zd_build(dev(pts))
+    assert_same_structure(t.zd_export(), oracle_mod.Tree(pts))
+    assert t.zd_size() == n
+
+
+@pytest.mark.parametrize("dist,dim", [("uniform", 2), ("uniform", 3), ("plummer", 3), ("sphere", 3),
+                                      ("dup", 2), ("dup", 3)])
+@pytest.mark.parametrize("leaf_max", [1, 4, 16, 32])
+def test_structure_distributions(zd, oracle_mod, dist, dim, leaf_max):
+    pts = zdgen.points(dist, 30000, dim, seed=7)
+    t = zd.zd_build(dev(pts), leaf_max=leaf_max)
+    assert_same_structure(t.zd_export(), oracle_mod.Tree(pts, leaf_max=leaf_max))
+
+
+@pytest.mark.parametrize("dist,dim", [("uniform", 2), ("uniform", 3), ("plummer", 3), ("sphere", 3),
+                                      ("dup", 2), ("dup", 3)])
+@pytest.mark.parametrize("k", [1, 3, 5, 10, 16, 32])
+def test_knn_all_distributions(zd, oracle_mod, dist, dim, k):
+    pts = zdgen.points(dist, 20000, dim, seed=11)
+    t = zd.zd_build(dev(pts))
+    gi, gd = gpu_knn_all(t, k)
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(k)
+    check_rows(gi, gd, oi, od)
+
+
+@pytest.mark.parametrize("leaf_max", [1, 2, 7, 16, 32])
+def test_knn_leaf_sizes(zd, oracle_mod, leaf_max):
+    pts = zdgen.points("plummer", 15000, 3, seed=3)
+    t = zd.zd_build(dev(pts), leaf_max=leaf_max)
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(10)
+    check_rows(gi, gd, oi, od)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 5, 11, 17])
+def test_knn_tiny_padding(zd, oracle_mod, n):
+    pts = zdgen.uniform(n, 3, seed=n)
+    t = zd.zd_build(dev(pts))
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(10)
+    check_rows(gi, gd, oi, od)
+    if n:
+        assert np.all(gi[:, max(n - 1, 0):] == -1)
+
+
+def test_lattices_every_row(zd, oracle_mod):
+    for side, dim in ((8, 3), (16, 2), (32, 2)):
+        pts = zdgen.grid(side, dim)
+        for k in (1, 6, 27):
+            t = zd.zd_build(dev(pts))
+            gi, gd = gpu_knn_all(t, k)
+            bi, bd = oracle_mod.brute_knn(pts, None, pts, np.arange(len(pts), dtype=np.int32), k)
+            check_rows(gi, gd, bi, bd)
+
+
+def test_c1_full_vs_brute_force(zd, oracle_mod):
+    """Config C1 (65,536 2D uniform, seed 1): every row vs plain brute force."""
+    pts = zdgen.config_points("C1")
+    t = zd.zd_build(dev(pts))
+    gi, gd = gpu_knn_all(t, 10)
+    bi, bd = oracle_mod.brute_knn(pts, None, pts, np.arange(len(pts), dtype=np.int32), 10)
+    check_rows(gi, gd, bi, bd)
+    assert_same_structure(t.zd_export(), oracle_mod.Tree(pts))
+
+
+def test_host_pointers_and_host_outputs(zd, oracle_mod):
+    """The C ABI accepts host arrays (staged internally) and host outputs."""
+    pts = zdgen.uniform(5000, 3, seed=5)
+    t = zd.zd_build(pts)                      # numpy host array
+    oi = np.empty((5000, 10), np.int32)
+    od = np.empty((5000, 10), np.int64)
+    t.zd_knn(10, out_idx=oi, out_dist2=od)     # host outputs, synchronous
+    ri, rd, _ = oracle_mod.Tree(pts).knn_all(10)
+    check_rows(oi, od, ri, rd)
+
+
+@pytest.mark.parametrize("dist,dim", [("uniform", 3), ("plummer", 3), ("uniform", 2), ("dup", 2)])
+@pytest.mark.parametrize("k", [1, 10, 32])
+def test_external_queries(zd, oracle_mod, dist, dim, k):
+    pts = zdgen.points(dist, 20000, dim, seed=21)
+    q = zdgen.uniform(3000, dim, seed=22)
+    if dist == "dup":
+        q = q % 8
+    if dist == "plummer":
+        q = np.concatenate([q, zdgen.plummer(3000, 23)])
+    t = zd.zd_build(dev(pts))
+    gi, gd = t.zd_knn(k, queries=dev(q))
+    torch.cuda.synchronize()
+    bi, bd = oracle_mod.brute_knn(pts, None, q, None, k)
+    check_rows(gi.cpu().numpy(), gd.cpu().numpy(), bi, bd)
+    oi, od, _ = oracle_mod.Tree(pts).knn_queries(q, k)
+    check_rows(gi.cpu().numpy(), gd.cpu().numpy(), oi, od)
+
+
+def test_external_queries_empty_tree(zd):
+    t = zd.zd_build(dev(np.zeros((0, 3), np.int32)))
+    gi, gd = t.zd_knn(4, queries=dev(np.array([[1, 2, 3]], np.int32)))
+    assert gi.cpu().tolist() == [[-1] * 4]
+    assert gd.cpu().tolist() == [[np.iinfo(np.int64).max] * 4]
+
+
+# ------------------------------------------------------------------ updates
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_insert_then_delete(zd, oracle_mod, dim):
+    base = zdgen.uniform(30000, dim, seed=31)
+    batch = zdgen.uniform(7000, dim, seed=32)
+    t = zd.zd_build(dev(base))
+    live = oracle_mod.LiveSet(base)
+    r0 = gpu_knn_all(t, 10)
+    first = t.zd_insert(dev(batch))
+    assert first == live.insert(batch) == 30000
+    assert t.zd_size() == 37000
+    assert_same_structure(t.zd_export(), live.tree())
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(gi, gd, oi, od)
+    # delete the batch: every original row is restored bit-exactly
+    assert t.zd_delete(dev(np.arange(30000, 37000, dtype=np.int32))) == 7000
+    r1 = gpu_knn_all(t, 10)
+    assert np.array_equal(r0[0], r1[0]) and np.array_equal(r0[1], r1[1])
+
+
+def test_delete_rows_and_live_ids(zd, oracle_mod):
+    base = zdgen.uniform(40000, 3, seed=41)
+    t = zd.zd_build(dev(base))
+    live = oracle_mod.LiveSet(base)
+    kill = zdgen.delete_ids(40000, 9000, seed=8)
+    dup = np.concatenate([kill, kill[:100], np.array([-1, 40000, 10 ** 9], np.int32)])
+    assert t.zd_delete(dev(dup)) == 9000 == live.delete(kill)
+    assert t.zd_delete(dev(kill[:10])) == 0           # already dead: skipped
+    assert np.array_equal(t.zd_live_ids().cpu().numpy(), live.live_ids())
+    assert_same_structure(t.zd_export(), live.tree())
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(gi, gd, oi, od)
+
+
+def test_update_sequence_mixed(zd, oracle_mod):
+    """Several rounds of insert / delete (C5 shape, small) stay canonical and exact."""
+    rng = np.random.default_rng(4)
+    base = zdgen.plummer(20000, 51)
+    t = zd.zd_build(dev(base))
+    live = oracle_mod.LiveSet(base)
+    for r in range(6):
+        b = zdgen.plummer(int(rng.integers(1, 5000)), 60 + r)
+        assert t.zd_insert(dev(b)) == live.insert(b)
+        ids = live.live_ids()
+        kill = rng.choice(ids, size=min(len(ids), int(rng.integers(0, 6000))), replace=False).astype(np.int32)
+        assert t.zd_delete(dev(kill)) == live.delete(kill)
+        assert t.zd_size() == len(live.ids)
+    assert_same_structure(t.zd_export(), live.tree())
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(gi, gd, oi, od)
+
+
+def test_insert_growth_and_delete_all(zd, oracle_mod):
+    base = zdgen.uniform(100, 2, seed=1)
+    t = zd.zd_build(dev(base))
+    live = oracle_mod.LiveSet(base)
+    for r in range(4):                                   # grows capacity several times
+        b = zdgen.uniform(300 * (r + 1), 2, seed=70 + r)
+        assert t.zd_insert(dev(b)) == live.insert(b)
+    assert_same_structure(t.zd_export(), live.tree())
+    assert t.zd_delete(dev(live.live_ids())) == len(live.ids)
+    assert t.zd_size() == 0
+    gi, gd = gpu_knn_all(t, 3)
+    assert gi.shape == (0, 3)
+    b = zdgen.uniform(50, 2, seed=99)
+    first = t.zd_insert(dev(b))
+    assert first == 100 + sum(300 * (r + 1) for r in range(4))
+
+
+# ------------------------------------------------------------------- errors
+
+def test_errors(zd):
+    bad = np.array([[0, 1 << 21, 5]], np.int32)
+    with pytest.raises(zd.ZdError) as e:
+        zd.zd_build(dev(bad))
+    assert e.value.code == zd.ZD_ERANGE
+    with pytest.raises(zd.ZdError) as e:
+        zd.zd_build(dev(np.array([[-1, 0]], np.int32)))
+    assert e.value.code == zd.ZD_ERANGE
+    pts = zdgen.uniform(1000, 3, seed=2)
+    t = zd.zd_build(dev(pts))
+    before = t.zd_export()
+    with pytest.raises(zd.ZdError) as e:
+        t.zd_insert(dev(np.concatenate([zdgen.uniform(10, 3, seed=3), bad])))
+    assert e.value.code == zd.ZD_ERANGE
+    after = t.zd_export()                            # all-or-nothing: unchanged
+    assert np.array_equal(before["recs"], after["recs"]) and t.zd_size() == 1000
+    assert t.zd_insert(dev(zdgen.uniform(1, 3, seed=4))) == 1000   # ids not consumed by the failed insert
+    for k in (0, 33):
+        with pytest.raises(zd.ZdError) as e:
+            t.zd_knn(k)
+        assert e.value.code == zd.ZD_EINVAL
+    with pytest.raises(zd.ZdError):
+        t.zd_knn(5, queries=dev(bad))
+    with pytest.raises(zd.ZdError):
+        zd.zd_build(dev(pts), leaf_max=33)
+
+
+def test_streams_and_timing(zd, oracle_mod):
+    pts = zdgen.uniform(50000, 3, seed=9)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        t = zd.zd_build(dev(pts), stream=s)
+        t.zd_set_timing(True)
+        oi, od = t.zd_knn(10)
+    s.synchronize()
+    tm = t.zd_get_timing()
+    assert tm["knn"] > 0
+    ri, rd, _ = oracle_mod.Tree(pts).knn_all(10)
+    check_rows(oi.cpu().numpy(), od.cpu().numpy(), ri, rd)
