@@ -166,6 +166,8 @@ ZD_API int zd_export(const zd_tree *h, uint64_t *keys, int32_t *recs, int32_t *l
  * returns the number filled.  Timing adds event records but no extra syncs
  * beyond the ones each call already makes (zd_knn syncs when timing is on). */
 ZD_API int zd_set_timing(zd_tree *h, int enable);
+/* Process-wide number of CUDA kernels this library has launched so far. */
+ZD_API int64_t zd_kernel_launches(void);
 ZD_API int zd_get_timing(const zd_tree *h, float *ms, int nphase);
 
 #ifdef __cplusplus

@@ -79,6 +79,8 @@ def load():
     L.zd_export.argtypes = [P, P, P, P, P, P]
     L.zd_set_timing.restype = i32
     L.zd_set_timing.argtypes = [P, i32]
+    L.zd_kernel_launches.restype = i64
+    L.zd_kernel_launches.argtypes = []
     L.zd_get_timing.restype = i32
     L.zd_get_timing.argtypes = [P, C.POINTER(C.c_float), i32]
     _lib = L
@@ -217,6 +219,11 @@ class ZdTree:
         return {PHASES[i]: float(buf[i]) for i in range(c)}
 
 
+def zd_kernel_launches() -> int:
+    """Process-wide number of CUDA kernels libzd.so has launched."""
+    return int(load().zd_kernel_launches())
+
+
 def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None, timing: bool = False) -> ZdTree:
     """Build a zd-tree over int32 points [n, dim] (point i gets id i)."""
     p = _as_i32(points)
@@ -232,5 +239,5 @@ def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None,
     return ZdTree(h, dim)
 
 
-__all__ = ["zd_build", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "PHASES",
+__all__ = ["zd_build", "zd_kernel_launches", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "PHASES",
            "ZD_OK", "ZD_EINVAL", "ZD_ERANGE", "ZD_ENOMEM", "ZD_ECUDA"]

@@ -5,7 +5,10 @@
 // pool (cudaMallocAsync) with the release threshold raised, so repeated builds and
 // updates reuse memory without device-wide synchronisation.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
+#include <mutex>
+#include <vector>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -14,6 +17,11 @@
 #include "internal.h"
 
 using namespace zd;
+
+namespace zd {
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+}  // namespace zd
 
 namespace {
 
@@ -83,6 +91,40 @@ template <class T>
 void dfree(T*& p, cudaStream_t st) {
     if (p) cudaFreeAsync(p, st);
     p = nullptr;
+}
+
+// Process-wide pinned host arena of small per-handle mailboxes (one cudaMallocHost
+// for the process instead of one per handle).
+struct PinnedSlots {
+    static constexpr int kSlots = 4096, kWords = 8;
+    std::mutex mu;
+    int32_t* base = nullptr;
+    std::vector<int> free_list;
+    int32_t* get() {
+        std::lock_guard<std::mutex> g(mu);
+        if (!base) {
+            if (cudaMallocHost((void**)&base, sizeof(int32_t) * kSlots * kWords) != cudaSuccess) {
+                cudaGetLastError();
+                base = nullptr;
+                return nullptr;
+            }
+            for (int i = kSlots - 1; i >= 0; --i) free_list.push_back(i);
+        }
+        if (free_list.empty()) return nullptr;
+        int s = free_list.back();
+        free_list.pop_back();
+        return base + (size_t)s * kWords;
+    }
+    bool put(int32_t* p) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!base || p < base || p >= base + (size_t)kSlots * kWords) return false;
+        free_list.push_back((int)((p - base) / kWords));
+        return true;
+    }
+};
+PinnedSlots& pinned() {
+    static PinnedSlots* p = new PinnedSlots();   // never destroyed (process lifetime)
+    return *p;
 }
 
 enum Phase { PH_SORT = 0, PH_TOPO = 1, PH_BBOX = 2, PH_MERGE = 3, PH_KNN = 4, PH_VALID = 5, NPH = 6 };
@@ -269,7 +311,7 @@ void destroy(zd_tree* h) {
     dfree(h->alive, h->st); dfree(h->row_of_id, h->st); dfree(h->live_ids, h->st); dfree(h->rank_cnt, h->st);
     dfree(h->d_small, h->st);
     cudaStreamSynchronize(h->st);
-    if (h->h_small) cudaFreeHost(h->h_small);
+    if (h->h_small && !pinned().put(h->h_small)) delete[] h->h_small;
     for (auto& e : h->ev) if (e) cudaEventDestroy(e);
     delete h;
 }
@@ -277,8 +319,9 @@ void destroy(zd_tree* h) {
 int do_build(zd_tree* h, const int32_t* points, int64_t n) {
     pool_setup_once();
     ZD_CUDA(dalloc(&h->d_small, 8, h->st));
-    ZD_CUDA(cudaMallocHost((void**)&h->h_small, 8 * sizeof(int32_t)));
-    for (auto& e : h->ev) ZD_CUDA(cudaEventCreate(&e));
+    h->h_small = pinned().get();
+    if (!h->h_small) h->h_small = new int32_t[8];
+    if (h->timing) for (auto& e : h->ev) ZD_CUDA(cudaEventCreate(&e));
     ZD_CUDA(cudaMemsetAsync(h->d_small, 0, 8 * sizeof(int32_t), h->st));
     const void* dpts = nullptr;
     void* owned = nullptr;
@@ -354,9 +397,13 @@ int zd_set_stream(zd_tree* h, void* stream) {
 
 int zd_set_timing(zd_tree* h, int enable) {
     if (!h) return fail(ZD_EINVAL, "NULL handle");
+    if (enable && !h->ev[0])
+        for (auto& e : h->ev) ZD_CUDA(cudaEventCreate(&e));
     h->timing = enable != 0;
     return ZD_OK;
 }
+
+int64_t zd_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int zd_get_timing(const zd_tree* h, float* ms, int nphase) {
     if (!h || !ms) return fail(ZD_EINVAL, "NULL argument");

@@ -7,6 +7,9 @@
 
 namespace zd {
 
+// process-wide count of kernel launches issued by this library (zd_kernel_launches)
+void count_launch(int k = 1);
+
 // ---------------------------------------------------------------- sort (sort.cu)
 // One-sweep LSD radix sort of (Morton key, id): 8 passes x 8-bit digits, one
 // up-front histogram of all 8 digits, decoupled look-back per pass.

@@ -237,6 +237,7 @@ template <int DIM, int K>
 void launch_all(const KnnArgs& a, cudaStream_t st) {
     Tree T{a.recs, a.leaf_start, a.leaf_parent, a.nodes};
     const int grid = (int)((a.n + 127) / 128);
+    if (grid > 0) count_launch(1);
     if (grid > 0)
         knn_all_kernel<DIM, K><<<grid, 128, 0, st>>>(T, a.pt_leaf, (int32_t)a.n, a.k, a.row_of_id, a.out_idx, a.out_d2);
 }
@@ -245,6 +246,7 @@ template <int DIM, int K>
 void launch_ext(const KnnArgs& a, const int32_t* queries, int64_t m, cudaStream_t st) {
     Tree T{a.recs, a.leaf_start, a.leaf_parent, a.nodes};
     const int grid = (int)((m + 127) / 128);
+    if (grid > 0) count_launch(1);
     if (grid > 0) knn_ext_kernel<DIM, K><<<grid, 128, 0, st>>>(T, a.d_meta, queries, (int32_t)m, a.k, a.out_idx, a.out_d2);
 }
 

@@ -207,6 +207,7 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
     int hb = (int)std::min<size_t>((size_t)sms * 8, (n + 255) / 256);
     hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid);
     scan_hist_kernel<<<1, 256, 0, st>>>(hist, s.offs);
+    count_launch(2 + NPASS);
     for (int p = 0; p < NPASS; ++p) {
         uint32_t* stp = status + (size_t)p * tiles * 256;
         const uint32_t* off = s.offs + p * 256;

@@ -182,16 +182,19 @@ void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, 
         // bookkeeping path with an empty pair range.
         cudaMemsetAsync(t.block_cnt, 0, 2 * sizeof(uint32_t), st);
         compact_kernel<<<1, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta, t.visit);
+        count_launch(1);
     } else {
         flags_kernel<<<nblk, TT, 0, st>>>(keys, un, leaf_max, t.flags, t.block_cnt);
         scan_blocks_kernel<<<1, 1024, 0, st>>>(t.block_cnt, (uint32_t)nblk);
         compact_kernel<<<nblk, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta, t.visit);
+        count_launch(3);
     }
     if (ev_mid) cudaEventRecord(ev_mid, st);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int grid = (int)std::min<int64_t>((int64_t)sms * 16, std::max<int64_t>(1, (n / 8 + 127) / 128));
+    count_launch(1);
     if (dim == 2)
         bottom_up_kernel<2><<<grid, 128, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<2>*)t.nodes,
                                                   t.leaf_parent, t.visit, t.range);

@@ -187,6 +187,7 @@ void validate_points(int dim, const int32_t* pts, int64_t m, int* d_invalid, cud
     const uint32_t lim = 1u << (dim == 2 ? Dim<2>::B : Dim<3>::B);
     const int grid = (int)std::min<int64_t>((int64_t)num_sms() * 4, (count + 255) / 256);
     validate_kernel<<<grid, 256, 0, st>>>(pts, count, lim, d_invalid);
+    count_launch(1);
 }
 
 void merge_sorted(const uint64_t* ka, const int4* ra, int64_t n, const uint64_t* kb, const int4* rb, int64_t m,
@@ -195,6 +196,7 @@ void merge_sorted(const uint64_t* ka, const int4* ra, int64_t n, const uint64_t*
     if (tot <= 0) return;
     const int64_t threads = (tot + MI - 1) / MI;
     merge_kernel<<<(unsigned)((threads + MT - 1) / MT), MT, 0, st>>>(ka, ra, n, kb, rb, m, ko, ro);
+    count_launch(1);
 }
 
 void set_alive_range(uint32_t* alive, int64_t first, int64_t count, cudaStream_t st) {
@@ -202,6 +204,7 @@ void set_alive_range(uint32_t* alive, int64_t first, int64_t count, cudaStream_t
     const int64_t words = ((first + count + 31) >> 5) - (first >> 5);
     const int grid = (int)std::min<int64_t>((int64_t)num_sms() * 4, (words + 255) / 256);
     set_alive_kernel<<<grid, 256, 0, st>>>(alive, first, count);
+    count_launch(1);
 }
 
 void mark_deleted(uint32_t* alive, int64_t id_cap, const int32_t* ids, int64_t m, unsigned long long* d_count,
@@ -209,6 +212,7 @@ void mark_deleted(uint32_t* alive, int64_t id_cap, const int32_t* ids, int64_t m
     if (m <= 0) return;
     const int grid = (int)std::min<int64_t>((int64_t)num_sms() * 4, (m + 255) / 256);
     mark_deleted_kernel<<<grid, 256, 0, st>>>(alive, id_cap, ids, m, d_count);
+    count_launch(1);
 }
 
 size_t compact_blocks(int64_t n) { return (size_t)std::max<int64_t>(1, (n + CTILE - 1) / CTILE); }
@@ -220,6 +224,7 @@ void compact_alive(const uint32_t* alive, const uint64_t* ki, const int4* ri, in
     compact_count_kernel<<<nb, CT, 0, st>>>(alive, ri, n, block_cnt);
     scan_blocks_kernel<<<1, 1024, 0, st>>>(block_cnt, (uint32_t)nb);
     compact_write_kernel<<<nb, CT, 0, st>>>(alive, ki, ri, n, block_cnt, ko, ro);
+    count_launch(3);
 }
 
 size_t rank_blocks(int64_t id_cap) { return (size_t)std::max<int64_t>(1, (((id_cap + 31) >> 5) + RT - 1) / RT); }
@@ -232,6 +237,7 @@ void rank_alive(const uint32_t* alive, int64_t id_cap, int32_t* row_of_id, int32
     rank_count_kernel<<<nb, RT, 0, st>>>(alive, words, block_cnt);
     scan_blocks_kernel<<<1, 1024, 0, st>>>(block_cnt, (uint32_t)nb);
     rank_write_kernel<<<nb, RT, 0, st>>>(alive, words, id_cap, block_cnt, row_of_id, live_ids);
+    count_launch(3);
 }
 
 }  // namespace zd
