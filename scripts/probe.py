@@ -1,9 +1,13 @@
 """Quick per-phase timing probe (development aid, not the bench contract)."""
 import argparse
 import json
+import sys
 import time
+from pathlib import Path
 
 import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 import paper_2111_04182_b200 as zd
 import zdgen
