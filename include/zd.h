@@ -170,6 +170,15 @@ ZD_API int zd_set_timing(zd_tree *h, int enable);
 ZD_API int64_t zd_kernel_launches(void);
 ZD_API int zd_get_timing(const zd_tree *h, float *ms, int nphase);
 
+/* Work counters accumulated by the k-NN kernel since the last reset, for profiling
+ * builds only (compiled with -DZD_KNN_STATS; a normal build returns ZD_EINVAL).
+ * Order: packets, queries, internal nodes visited, stack pops, ascents, scanned
+ * spans, uniform passes, candidates tested (per warp), hits (sum over lanes),
+ * hit rounds (max over lanes per pass), compactions, final survivors (sum over
+ * lanes), final survivors (max over lanes per packet).  Fills min(n, 13) int64
+ * entries, returns the number filled; reset != 0 zeroes the counters after reading. */
+ZD_API int zd_knn_stats(int64_t *out, int n, int reset);
+
 #ifdef __cplusplus
 }
 #endif

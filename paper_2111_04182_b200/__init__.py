@@ -16,7 +16,10 @@ from typing import Optional
 
 import numpy as np
 
-from ._build import LIB_PATH, build_lib
+import os
+from pathlib import Path
+
+from ._build import LIB_PATH, STATS_LIB_PATH, build_lib
 
 ZD_OK, ZD_EINVAL, ZD_ERANGE, ZD_ENOMEM, ZD_ECUDA = 0, -1, -2, -3, -4
 ZD_K_MAX = 32
@@ -43,13 +46,15 @@ class _Info(C.Structure):
 
 
 def load():
-    """Load libzd.so (no rebuild on the GPU box unless sources are newer)."""
+    """Load libzd.so (never rebuilt here).  ZD_LIB=stats selects the profiling variant
+    libzd_stats.so (work counters, zd_knn_stats)."""
     global _lib
     if _lib is not None:
         return _lib
-    if not LIB_PATH.exists():
-        raise RuntimeError(f"libzd.so not built ({LIB_PATH}); run __graft_entry__.build()")
-    L = C.CDLL(str(LIB_PATH))
+    path = STATS_LIB_PATH if os.environ.get("ZD_LIB") == "stats" else LIB_PATH
+    if not path.exists():
+        raise RuntimeError(f"{path.name} not built ({path}); run __graft_entry__.build()")
+    L = C.CDLL(str(path))
     P, i64, i32 = C.c_void_p, C.c_int64, C.c_int
     L.zd_build.restype = P
     L.zd_build.argtypes = [P, i64, i32]
@@ -83,6 +88,8 @@ def load():
     L.zd_kernel_launches.argtypes = []
     L.zd_get_timing.restype = i32
     L.zd_get_timing.argtypes = [P, C.POINTER(C.c_float), i32]
+    L.zd_knn_stats.restype = i32
+    L.zd_knn_stats.argtypes = [P, i32, i32]
     _lib = L
     return L
 
@@ -219,6 +226,17 @@ class ZdTree:
         return {PHASES[i]: float(buf[i]) for i in range(c)}
 
 
+KNN_STATS = ("packets", "queries", "nodes", "pops", "ascents", "spans", "passes", "candidates", "hits",
+             "rounds", "compactions", "survivors", "survivors_max")
+
+
+def zd_knn_stats(reset: bool = True) -> dict:
+    """Work counters of the k-NN kernel (profiling build only, ZD_LIB=stats)."""
+    out = np.zeros(len(KNN_STATS), np.int64)
+    n = _check(load().zd_knn_stats(_ptr(out), len(KNN_STATS), int(reset)))
+    return dict(zip(KNN_STATS[:n], out[:n].tolist()))
+
+
 def zd_kernel_launches() -> int:
     """Process-wide number of CUDA kernels libzd.so has launched."""
     return int(load().zd_kernel_launches())
@@ -239,5 +257,5 @@ def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None,
     return ZdTree(h, dim)
 
 
-__all__ = ["zd_build", "zd_kernel_launches", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "PHASES",
+__all__ = ["zd_build", "zd_kernel_launches", "zd_knn_stats", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "PHASES",
            "ZD_OK", "ZD_EINVAL", "ZD_ERANGE", "ZD_ENOMEM", "ZD_ECUDA"]

@@ -10,6 +10,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_PATH = PKG / "libzd.so"
+STATS_LIB_PATH = PKG / "libzd_stats.so"   # profiling variant (-DZD_KNN_STATS work counters)
 SOURCES = ["sort.cu", "tree.cu", "knn.cu", "update.cu", "api.cu"]
 DEPS = SOURCES + ["common.cuh", "internal.h"]
 
@@ -28,21 +29,23 @@ def _nvcc() -> str:
     return "nvcc"
 
 
-def stale() -> bool:
-    if not LIB_PATH.exists():
+def stale(path: Path = LIB_PATH) -> bool:
+    if not path.exists():
         return True
-    t = LIB_PATH.stat().st_mtime
+    t = path.stat().st_mtime
     deps = [CSRC / f for f in DEPS] + [ROOT / "include" / "zd.h"]
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
-        return LIB_PATH
-    tmp = LIB_PATH.with_name(f"libzd.so.tmp{os.getpid()}")
-    cmd = [_nvcc(), *NVCC_FLAGS, *[str(CSRC / s) for s in SOURCES], "-o", str(tmp)]
+def build_lib(force: bool = False, verbose: bool = False, stats: bool = False) -> Path:
+    path = STATS_LIB_PATH if stats else LIB_PATH
+    if not force and not stale(path):
+        return path
+    tmp = path.with_name(f"{path.name}.tmp{os.getpid()}")
+    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DZD_KNN_STATS"] if stats else []),
+           *[str(CSRC / s) for s in SOURCES], "-o", str(tmp)]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd, cwd=str(CSRC))
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, path)
+    return path

@@ -405,6 +405,14 @@ int zd_set_timing(zd_tree* h, int enable) {
 
 int64_t zd_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
+int zd_knn_stats(int64_t* out, int n, int reset) {
+    clear_err();
+    if (!out || n < 0) return fail(ZD_EINVAL, "zd_knn_stats: bad arguments");
+    const int r = knn_stats(reinterpret_cast<unsigned long long*>(out), n, reset);
+    if (r < 0) return fail(ZD_EINVAL, "zd_knn_stats: not a -DZD_KNN_STATS build");
+    return r;
+}
+
 int zd_get_timing(const zd_tree* h, float* ms, int nphase) {
     if (!h || !ms) return fail(ZD_EINVAL, "NULL argument");
     int c = std::min(nphase, (int)NPH);
@@ -431,7 +439,9 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
     KnnArgs a{};
     a.dim = h->dim; a.k = k; a.n = h->n;
     a.recs = h->recs; a.pt_leaf = h->tb.pt_leaf; a.leaf_start = h->tb.leaf_start;
-    a.leaf_parent = h->tb.leaf_parent; a.nodes = h->tb.nodes; a.d_meta = h->d_small;
+    a.leaf_parent = h->tb.leaf_parent; a.nodes = h->tb.nodes; a.node_range = h->tb.range;
+    a.split_bit = h->tb.split_bit;
+    a.d_meta = h->d_small;
     a.out_idx = di; a.out_d2 = dd;
     if (!queries) {
         if ((rc = ensure_rows(h))) return rc;
@@ -453,11 +463,23 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
             if (host_out) { dfree(di, h->st); dfree(dd, h->st); }
             return fail(ZD_ERANGE, "zd_knn: query outside the universe box");
         }
+        // Morton-sort the queries (K1/K2; ids = query index), locate their leaves by
+        // their key bits and run the packet search in Morton order
+        uint64_t* qk = nullptr;
+        int4* qr = nullptr;
+        int32_t* ql = nullptr;
+        ZD_CUDA(dalloc(&qk, m, h->st));
+        ZD_CUDA(dalloc(&qr, m, h->st));
+        ZD_CUDA(dalloc(&ql, m, h->st));
         rec(h, 0);
-        knn_queries(a, (const int32_t*)dq, m, nullptr, h->st);
+        if ((rc = sort_into(h, (const int32_t*)dq, m, 0, qk, qr))) return rc;
+        knn_queries(a, qk, qr, ql, m, h->st);
         ZD_CHECK_LAUNCH("knn_queries");
         rec(h, 1);
         if (owned) cudaFreeAsync(owned, h->st);
+        dfree(qk, h->st);
+        dfree(qr, h->st);
+        dfree(ql, h->st);
     }
     if (host_out) {
         ZD_CUDA(cudaMemcpyAsync(out_idx, di, (size_t)m * k * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
@@ -616,8 +638,15 @@ int zd_export(const zd_tree* hc, uint64_t* keys, int32_t* recs, int32_t* leaf_st
     if (recs && h->n) ZD_CUDA(cudaMemcpyAsync(recs, h->recs, h->n * sizeof(int4), K, h->st));
     if (leaf_start) ZD_CUDA(cudaMemcpyAsync(leaf_start, h->tb.leaf_start, (h->n_leaves + 1) * sizeof(int32_t), K, h->st));
     if (leaf_parent) ZD_CUDA(cudaMemcpyAsync(leaf_parent, h->tb.leaf_parent, h->n_leaves * sizeof(int32_t), K, h->st));
-    if (nodes && h->n_internal)
-        ZD_CUDA(cudaMemcpyAsync(nodes, h->tb.nodes, h->n_internal * (h->dim == 2 ? 48 : 64), K, h->st));
+    if (nodes && h->n_internal) {
+        const size_t bytes = (size_t)h->n_internal * (4 * h->dim + 4) * sizeof(int32_t);
+        int32_t* tmp = nullptr;
+        ZD_CUDA(cudaMallocAsync((void**)&tmp, bytes, h->st));
+        export_nodes(h->dim, h->tb.nodes, h->tb.split_bit, h->n_internal, tmp, h->st);
+        ZD_CHECK_LAUNCH("export_nodes");
+        ZD_CUDA(cudaMemcpyAsync(nodes, tmp, bytes, K, h->st));
+        ZD_CUDA(cudaFreeAsync(tmp, h->st));
+    }
     ZD_CUDA(cudaStreamSynchronize(h->st));
     return ZD_OK;
 }

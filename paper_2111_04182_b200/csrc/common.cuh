@@ -84,11 +84,17 @@ template <int DIM> __device__ __forceinline__ bool in_universe(int x, int y, int
 // Internal node i (in-order: between leaf i and leaf i+1).  Both children's tight
 // bounding boxes live in the parent so one 48/64-byte load decides the visit
 // order and pruning of both children (Alg. 2's withinBox + nearer-child rule).
-// Child ref >= 0: internal node; < 0: leaf ~ref.
+// Child refs: >= 0 an internal node; < 0 a leaf, encoded by its sorted point range
+// so a leaf scan needs no further lookup:
+//   left  leaf (= leaf i)   : left  = ~start, points [start, mid)
+//   right leaf (= leaf i+1) : right = ~end,   points [mid, end)
+// mid = first sorted position of the right subtree (= leaf_start[i+1]).  The split
+// bit lives in a separate array (TreeBufs::split_bit); zd_export converts to the
+// documented leaf-index form.
 template <int DIM> struct alignas(16) Node {
     int32_t lbox[2 * DIM];   // lo[DIM], hi[DIM]
     int32_t rbox[2 * DIM];
-    int32_t left, right, parent, split;
+    int32_t left, right, parent, mid;
 };
 static_assert(sizeof(Node<2>) == 48, "Node<2> layout");
 static_assert(sizeof(Node<3>) == 64, "Node<3> layout");

@@ -45,6 +45,9 @@ size_t tree_blocks(int64_t n);
 // Canonical topology (K4) + bottom-up boxes (K5) over sorted keys/records.
 void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, int leaf_max,
                     const TreeBufs& t, cudaStream_t st, cudaEvent_t ev_mid);
+// Internal nodes in the documented zd_export layout (leaf children as ~leaf index,
+// split bit last) into out int32 [nb][4*dim+4].
+void export_nodes(int dim, const void* nodes, const int32_t* split_bit, int64_t nb, int32_t* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- knn (knn.cu)
 struct KnnArgs {
@@ -55,15 +58,23 @@ struct KnnArgs {
     const int32_t* leaf_start;
     const int32_t* leaf_parent;
     const void* nodes;
+    const int32_t* node_range;   // [2*n_internal]: leaves [L, R] under internal node i
+    const int32_t* split_bit;    // [n_internal]
     const int32_t* d_meta;       // root ref at [1]
     const int32_t* row_of_id;    // NULL: row = id
     int32_t* out_idx;
     int64_t* out_d2;
 };
 int knn_kmax();
+// Work counters of the packet k-NN kernel (only in a -DZD_KNN_STATS build).
+enum { ZS_PACKETS = 0, ZS_QUERIES, ZS_NODES, ZS_POPS, ZS_ASCENTS, ZS_SPANS, ZS_PASSES, ZS_CAND, ZS_HITS,
+       ZS_ROUNDS, ZS_COMPACT, ZS_SURV, ZS_SURV_MAX, ZD_NSTATS };
+int knn_stats(unsigned long long* out, int n, int reset);
 void knn_all(const KnnArgs& a, cudaStream_t st);
-// External queries: pts int32 [m][dim] (validated), bit-based leaf location.
-void knn_queries(const KnnArgs& a, const int32_t* queries, int64_t m, int* d_invalid, cudaStream_t st);
+// External queries, already Morton-sorted (qkeys, qrecs with w = query index):
+// bit-based leaf location into qleaf [m], then the packet search (row = query index).
+void knn_queries(const KnnArgs& a, const uint64_t* qkeys, const int4* qrecs, int32_t* qleaf, int64_t m,
+                 cudaStream_t st);
 
 // ---------------------------------------------------------------- updates (update.cu)
 void validate_points(int dim, const int32_t* pts, int64_t m, int* d_invalid, cudaStream_t st);

@@ -1,28 +1,54 @@
-// knn.cu — K6 exact k-NN over the zd-tree.
+// knn.cu — K6 exact k-NN over the zd-tree: warp-cooperative ("packet") searchUp.
 //
-// All-points ("leaf-based"): for every live point q, in sorted
-// (Morton) order so that neighbouring threads walk neighbouring subtrees:
-//   scan q's leaf, then Alg. 3 searchUp: while C has a parent and the
-//   k-ball may leave C, run Alg. 2 searchDown on C's sibling, C = parent.
-// External queries ("bit-based"): locate the leaf by the query's Morton bits
-// from the root, then the same searchUp; nothing is excluded.
+// PAPER.md: Alg. 3 searchUp calling Alg. 2 searchDown;
+// leaf-based all-points search; bit-based location of external queries
+// ("dynamic queries" P:183, App. B); queries walked in Morton order for
+// locality.
 //
-// Exact rules:
-//  * k-best set sorted by (d2, id) in registers (reading 14); a candidate enters iff
-//    (d2, id) < the current k-th (reading 11: insert the candidate, not p).
-//  * prune a subtree iff boxd2(q, box) > d2 of the k-th (strict; reading 8) — the
-//    set starts filled with (INT64_MAX, -1) so "|N| < k" needs no extra test.
-//  * stop ascending at C iff q is inside C's tight box and (m+1)^2 > k-th d2,
-//    m = min over axes of min(q - lo, hi - q) (reading 9): every point outside
-//    subtree(C) lies outside C's Morton cell, which contains the box.
-//  * self excluded by id (reading 13); nearer child first by box distance, tie -> left
-//    (reading 10; performance only — the answer is unique).
+// A warp owns a PACKET of 32 queries adjacent in Morton order (all-points: 32
+// consecutive sorted positions; external: 32 consecutive Morton-sorted queries),
+// whose leaves span lA..lB.  The warp runs ONE searchUp for the packet, each lane
+// keeping its own k-best state:
+//   1. scan leaves lA..lB (Alg. 3's leaf seed, for all lanes at once);
+//   2. if lA != lB, searchDown over the rest of the subtree of X = lowest common
+//      ancestor of lA and lB (leaves lA..lB skipped);
+//   3. ascend from X: stop when EVERY lane's stop test holds at C (reading 9), else
+//      searchDown the sibling of C, C = parent(C).
+// searchDown is joint: a subtree is entered iff SOME lane's box distance is <= its
+// bound (reading 8 per lane); nearer child first by lane majority (reading 10); the
+// far child goes on a per-warp shared-memory stack with its box and is re-tested
+// when popped.  Leaf points are staged through shared memory (coalesced 16-B loads,
+// one record per lane) and broadcast to all lanes; a node whose children are both
+// leaves is scanned as ONE contiguous span (its points are adjacent in sorted order).
+//
+// Per-lane k-best state (the warp never serialises on sorted insertions):
+//   fa[K]  ascending list of the k smallest d2 seen so far, each rounded UP to fp32
+//          (ids ignored), kept with branch-free min/max;
+//   U      = ceil(fa[K-1]) as int64: an upper bound on the exact k-th smallest d2 among
+//          the candidates seen, hence on the final k-th distance; U never grows;
+//   buf    (position, ru(d2)) of every candidate that had d2 <= U when seen.
+// A subtree or candidate can hold a final neighbour only if its (box) d2 <= U, so
+// pruning by "> U" (reading 8), stopping by "(m+1)^2 > U" (reading 9) and buffering
+// by "d2 <= U" lose nothing.  The buffer is compacted by ru(d2) <= fa[K-1] (sound:
+// rounding up is monotone), and at the end the ~k survivors are inserted exactly by
+// (d2, id) (reading 14) into a register list.  Every lane's answer is exact: it sees
+// a superset of what its own searchUp would see and drops a point only by its own
+// sound rules; the (d2, id) order makes the answer unique.  Self is excluded by id
+// (reading 13); short rows are padded with (-1, INT64_MAX) (reading 15).
 #include <climits>
 
 #include "common.cuh"
 #include "internal.h"
 
 namespace zd {
+
+// Optional work counters (build with -DZD_KNN_STATS; see zd_knn_stats in zd.h).
+#ifdef ZD_KNN_STATS
+__device__ unsigned long long g_knn_stats[ZD_NSTATS];
+#define ZD_STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_knn_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define ZD_STAT(i, v) do { } while (0)
+#endif
 
 namespace {
 
@@ -34,7 +60,6 @@ struct KBest {
 #pragma unroll
         for (int s = 0; s < K; ++s) { d[s] = INT64_MAX; i[s] = -1; }
     }
-    __device__ __forceinline__ int64_t worst() const { return d[K - 1]; }
     __device__ __forceinline__ bool accepts(int64_t cd, int32_t ci) const {
         return cd < d[K - 1] || (cd == d[K - 1] && ci < i[K - 1]);
     }
@@ -62,35 +87,38 @@ struct Query {
 
 template <int DIM>
 __device__ __forceinline__ int64_t dist2(const Query<DIM>& q, const int4& r) {
-    int dx = q.c[0] - r.x, dy = q.c[1] - r.y;
+    const int dx = q.c[0] - r.x, dy = q.c[1] - r.y;
     int64_t s = (int64_t)dx * dx + (int64_t)dy * dy;
     if (DIM == 3) {
-        int dz = q.c[2] - r.z;
+        const int dz = q.c[2] - r.z;
         s += (int64_t)dz * dz;
     }
     return s;
 }
 
+// squared distance from q to the box (lo[DIM], hi[DIM]); 0 inside (withinBox)
 template <int DIM>
 __device__ __forceinline__ int64_t boxd2(const Query<DIM>& q, const int32_t* b) {
     int64_t s = 0;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) {
-        int t = max(b[a] - q.c[a], 0) + max(q.c[a] - b[DIM + a], 0);
+        const int t = max(b[a] - q.c[a], 0) + max(q.c[a] - b[DIM + a], 0);
         s += (int64_t)t * t;
     }
     return s;
 }
 
-// stop test of Alg. 3 (reading 9); false when q is outside the box (external queries)
+// Alg. 3 stop test on C's tight box (reading 9): q inside the box with margin m on
+// every axis, (m+1)^2 > U.  Every point outside subtree(C) lies outside C's Morton
+// cell, which contains the box, so it is at least m+1 away on some axis.
 template <int DIM>
-__device__ __forceinline__ bool stop_at(const Query<DIM>& q, const int32_t* b, int64_t worst) {
+__device__ __forceinline__ bool stop_at(const Query<DIM>& q, const int32_t* b, int64_t U) {
     int m = INT_MAX;
 #pragma unroll
     for (int a = 0; a < DIM; ++a) m = min(m, min(q.c[a] - b[a], b[DIM + a] - q.c[a]));
     if (m < 0) return false;
     const int64_t mm = (int64_t)m + 1;
-    return mm * mm > worst;
+    return mm * mm > U;
 }
 
 template <int DIM>
@@ -103,165 +131,400 @@ __device__ __forceinline__ Node<DIM> load_node(const Node<DIM>* p) {
     return r;
 }
 
-struct Tree {
-    const int4* recs;
-    const int32_t* leaf_start;
-    const int32_t* leaf_parent;
-    const void* nodes;
+template <int K>
+struct Pw {
+    static constexpr int v = K <= 16 ? 4 : 2;   // warps per block (shared memory grows with K)
+};
+constexpr int CH = 16;                   // candidates tested per uniform pass
+constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
+
+template <int K>
+struct Cap {
+    static constexpr int v = (K + CH > 32) ? K + CH : 32;   // buffered candidates per lane
+};
+
+// A child reference in traversal form: ref >= 0 internal node; ref < 0 a leaf with
+// points [~ref, end).
+struct Ref {
+    int32_t ref, end;
+};
+
+template <int DIM>
+__device__ __forceinline__ Ref left_child(const Node<DIM>& nd) { return Ref{nd.left, nd.mid}; }
+template <int DIM>
+__device__ __forceinline__ Ref right_child(const Node<DIM>& nd) {
+    return nd.right >= 0 ? Ref{nd.right, 0} : Ref{~nd.mid, ~nd.right};
+}
+
+struct alignas(16) StkEntry {
+    int4 a, b;          // a = (ref, box words 0..2), b = (box words 3..5, leaf end)
+};
+
+template <int K>
+struct WarpSh {
+    int4 c[32];                          // staged candidates (x, y, z|0, id)
+    int32_t bp[Cap<K>::v][32];           // per-lane buffered positions; column = lane
+    float bf[Cap<K>::v][32];             //   ... and their d2 rounded up to fp32
+    StkEntry stk[kMaxDepth];
 };
 
 template <int DIM, int K>
-__device__ __forceinline__ void scan_leaf(const Tree& T, int32_t l, const Query<DIM>& q, KBest<K>& best) {
-    const int32_t s = __ldg(T.leaf_start + l), e = __ldg(T.leaf_start + l + 1);
-    for (int32_t j = s; j < e; ++j) {
-        const int4 r = __ldg(T.recs + j);
-        if (r.w == q.id) continue;
-        const int64_t d = dist2<DIM>(q, r);
-        if (best.accepts(d, r.w)) best.insert(d, r.w);
+struct Lane {
+    Query<DIM> q;
+    float fa[K];
+    int64_t U;          // -1 for an idle lane: needs nothing, accepts nothing
+    int cnt;
+};
+
+template <int DIM, int K>
+__device__ __forceinline__ void set_bound(Lane<DIM, K>& L) {
+    const float f = L.fa[K - 1];
+    L.U = (f == INFINITY) ? INT64_MAX : __float2ll_ru(f);
+}
+
+// Drop buffered candidates that can no longer qualify: a final neighbour p has
+// d2(p) <= the exact k-th smallest d2 seen so far, hence ru(d2(p)) <= fa[K-1].
+template <int DIM, int K>
+__device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
+    const float F = L.fa[K - 1];
+    int w = 0;
+    for (int e = 0; e < L.cnt; ++e) {
+        const float f = S.bf[e][lane];
+        const int32_t p = S.bp[e][lane];
+        S.bf[w][lane] = f;
+        S.bp[w][lane] = p;
+        w += (f <= F) ? 1 : 0;
+    }
+    L.cnt = w;
+}
+
+// Rare path (massive distance ties survive compaction): keep only the exact K best
+// buffered candidates by (d2, id).  Entries ranked >= K are marked +inf and dropped
+// by the next compaction; the K kept ones all have ru(d2) <= fa[K-1], so later
+// compactions keep them.  (Arguments by value: no Lane round trip through memory.)
+template <int DIM, int K>
+__device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Query<DIM> q, int cnt, WarpSh<K>& S,
+                                               int lane) {
+    for (int e = 0; e < cnt; ++e) {
+        const int4 ce = __ldg(recs + S.bp[e][lane]);
+        const int64_t de = dist2<DIM>(q, ce);
+        int rank = 0;
+        for (int f = 0; f < cnt; ++f) {
+            const int4 cf = __ldg(recs + S.bp[f][lane]);
+            const int64_t dv = dist2<DIM>(q, cf);
+            rank += (dv < de || (dv == de && cf.w < ce.w)) ? 1 : 0;
+        }
+        if (rank >= K) S.bf[e][lane] = INFINITY;
     }
 }
 
-// Alg. 2 searchDown on subtree `sub` whose box is sbox (explicit stack of far children)
+// Every lane scans sorted positions [s, e): up to 32 records at a time are staged
+// through shared memory, each lane tests CH of them per uniform pass against its
+// bound, then handles its (few) hits.
 template <int DIM, int K>
-__device__ __forceinline__ void search_down(const Tree& T, int32_t sub, const int32_t* sbox, const Query<DIM>& q,
-                                            KBest<K>& best) {
-    if (boxd2<DIM>(q, sbox) > best.worst()) return;
-    const Node<DIM>* nodes = static_cast<const Node<DIM>*>(T.nodes);
-    int32_t stk_ref[kMaxDepth];
-    int64_t stk_d[kMaxDepth];
-    int sp = 0;
-    int32_t cur = sub;
-    while (true) {
-        if (is_leaf_ref(cur)) {
-            scan_leaf<DIM, K>(T, ~cur, q, best);
-        } else {
-            const Node<DIM> nd = load_node<DIM>(nodes + cur);
-            const int64_t dl = boxd2<DIM>(q, nd.lbox), dr = boxd2<DIM>(q, nd.rbox);
-            const bool lfirst = dl <= dr;
-            const int64_t dn = lfirst ? dl : dr, df = lfirst ? dr : dl;
-            const int64_t w = best.worst();
-            if (dn <= w) {
-                if (df <= w) {
-                    stk_ref[sp] = lfirst ? nd.right : nd.left;
-                    stk_d[sp] = df;
-                    ++sp;
+__device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t s, int32_t e, Lane<DIM, K>& L,
+                                          WarpSh<K>& S, int lane) {
+    ZD_STAT(ZS_SPANS, 1);
+    for (int32_t b = s; b < e; b += 32) {
+        const int n32 = min(32, e - b);
+        __syncwarp();
+        if (lane < n32) S.c[lane] = __ldg(recs + b + lane);
+        __syncwarp();
+        for (int h0 = 0; h0 < n32; h0 += CH) {
+            const int cnt = min(CH, n32 - h0);
+            if (__any_sync(0xffffffffu, L.cnt + cnt > Cap<K>::v)) {
+                ZD_STAT(ZS_COMPACT, 1);
+                compact<DIM, K>(L, S, lane);
+                if (L.cnt + cnt > Cap<K>::v) {
+                    mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
+                    compact<DIM, K>(L, S, lane);
                 }
-                cur = lfirst ? nd.left : nd.right;
-                continue;
+            }
+            const int64_t U = L.U;
+            uint32_t hit = 0;
+#pragma unroll 4
+            for (int j = 0; j < cnt; ++j) {
+                const int4 c = S.c[h0 + j];
+                const bool h = dist2<DIM>(L.q, c) <= U && c.w != L.q.id;   // self excluded by id
+                hit |= (h ? 1u : 0u) << j;
+            }
+#ifdef ZD_KNN_STATS
+            {
+                ZD_STAT(ZS_CAND, cnt);
+                ZD_STAT(ZS_PASSES, 1);
+                int hc = __popc(hit), hm = hc;
+                for (int o = 16; o > 0; o >>= 1) { hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o)); hc += __shfl_xor_sync(0xffffffffu, hc, o); }
+                ZD_STAT(ZS_HITS, hc);
+                ZD_STAT(ZS_ROUNDS, hm);
+            }
+#endif
+            while (hit) {
+                const int j = h0 + __ffs(hit) - 1;
+                hit &= hit - 1;
+                const int64_t d = dist2<DIM>(L.q, S.c[j]);
+                if (d > L.U) continue;   // the bound shrank since the uniform pass
+                const float xf = __ll2float_ru(d);
+                float x = xf;
+#pragma unroll
+                for (int t = 0; t < K; ++t) {
+                    const float lo = fminf(L.fa[t], x);
+                    x = fmaxf(L.fa[t], x);
+                    L.fa[t] = lo;
+                }
+                set_bound<DIM, K>(L);
+                S.bp[L.cnt][lane] = b + j;
+                S.bf[L.cnt][lane] = xf;
+                ++L.cnt;
             }
         }
-        bool more = false;
-        while (sp > 0) {
-            --sp;
-            if (stk_d[sp] <= best.worst()) { cur = stk_ref[sp]; more = true; break; }
-        }
-        if (!more) break;
     }
 }
 
-// Alg. 3 searchUp from leaf l
+// scan [s, e) minus the already scanned span [ps_lo, ps_hi) (a union of whole leaves)
 template <int DIM, int K>
-__device__ __forceinline__ void search_up(const Tree& T, int32_t l, const Query<DIM>& q, KBest<K>& best) {
-    const Node<DIM>* nodes = static_cast<const Node<DIM>*>(T.nodes);
-    scan_leaf<DIM, K>(T, l, q, best);
-    int32_t C = ~l;
-    int32_t P = __ldg(T.leaf_parent + l);
-    while (P >= 0) {
+__device__ __forceinline__ void scan_leaves(const int4* __restrict__ recs, int32_t s, int32_t mid, int32_t e,
+                                            int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
+    // [s, mid) and [mid, e) are whole leaves (mid == e for a single leaf)
+    const bool skip_l = s >= ps_lo && s < ps_hi;
+    const bool skip_r = mid < e && mid >= ps_lo && mid < ps_hi;
+    const int32_t a = skip_l ? mid : s, b = skip_r ? mid : e;
+    if (a < b) scan_span<DIM, K>(recs, a, b, L, S, lane);
+}
+
+template <int DIM>
+__device__ __forceinline__ void unpack_box(const StkEntry& e, int32_t (&bx)[2 * DIM]) {
+    const int w[6] = {e.a.y, e.a.z, e.a.w, e.b.x, e.b.y, e.b.z};
+#pragma unroll
+    for (int a = 0; a < 2 * DIM; ++a) bx[a] = w[a];
+}
+
+// Joint Alg. 2 over the subtree `cur`; the span [ps_lo, ps_hi) was scanned already.
+template <int DIM, int K>
+__device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const Node<DIM>* __restrict__ nodes, Ref cur,
+                                           int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
+    int sp = 0;
+    while (true) {
+        bool descend = false;
+        if (cur.ref < 0) {
+            scan_leaves<DIM, K>(recs, ~cur.ref, cur.end, cur.end, ps_lo, ps_hi, L, S, lane);
+        } else {
+            ZD_STAT(ZS_NODES, 1);
+            const Node<DIM> nd = load_node<DIM>(nodes + cur.ref);
+            const int64_t w = L.U;
+            const int64_t dl = boxd2<DIM>(L.q, nd.lbox), dr = boxd2<DIM>(L.q, nd.rbox);
+            const bool nl = __any_sync(0xffffffffu, dl <= w), nr = __any_sync(0xffffffffu, dr <= w);
+            if (nl && nr && nd.left < 0 && nd.right < 0) {
+                // two leaf children: one contiguous span [start, end) of <= 2 leaves
+                scan_leaves<DIM, K>(recs, ~nd.left, nd.mid, ~nd.right, ps_lo, ps_hi, L, S, lane);
+            } else if (nl && nr) {
+                // visit first the child nearer for most lanes (performance only, reading 10)
+                const bool lfirst = __popc(__ballot_sync(0xffffffffu, dl <= dr)) >= 16;
+                const Ref far = lfirst ? right_child<DIM>(nd) : left_child<DIM>(nd);
+                __syncwarp();
+                if (lane == 0) {
+                    int w6[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+                    for (int a = 0; a < 2 * DIM; ++a) w6[a] = lfirst ? nd.rbox[a] : nd.lbox[a];
+                    StkEntry e;
+                    e.a = make_int4(far.ref, w6[0], w6[1], w6[2]);
+                    e.b = make_int4(w6[3], w6[4], w6[5], far.end);
+                    S.stk[sp] = e;
+                }
+                ++sp;
+                cur = lfirst ? left_child<DIM>(nd) : right_child<DIM>(nd);
+                descend = true;
+            } else if (nl || nr) {
+                cur = nl ? left_child<DIM>(nd) : right_child<DIM>(nd);
+                descend = true;
+            }
+        }
+        if (descend) continue;
+        // pop the next far child that some lane still needs
+        bool found = false;
+        __syncwarp();
+        while (sp > 0) {
+            --sp;
+            ZD_STAT(ZS_POPS, 1);
+            const StkEntry e = S.stk[sp];
+            int32_t bx[2 * DIM];
+            unpack_box<DIM>(e, bx);
+            if (__any_sync(0xffffffffu, boxd2<DIM>(L.q, bx) <= L.U)) {
+                cur = Ref{e.a.x, e.b.w};
+                found = true;
+                break;
+            }
+        }
+        if (!found) break;
+    }
+}
+
+struct PacketArgs {
+    const int4* recs;          // tree records (sorted)
+    const int32_t* leaf_start;
+    const int32_t* leaf_parent;
+    const void* nodes;
+    const int32_t* node_range;
+    const int4* qrecs;         // queries in Morton order: (x, y, z|0, id or query index)
+    const int32_t* qleaf;      // leaf of each query
+    int32_t nq;
+    int k;
+    const int32_t* row_of_id;  // all-points: row of an id (NULL: row = id)
+    int32_t* out_idx;
+    int64_t* out_d2;
+};
+
+// EXT = false: all-points (queries are the tree's own points; self excluded by id,
+// row = row_of_id[id]).  EXT = true: external queries (nothing excluded, row = query
+// index carried in the record's w).
+template <int DIM, int K, bool EXT>
+__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? 4 : 2)) knn_packet_kernel(PacketArgs A) {
+    __shared__ WarpSh<K> sh[Pw<K>::v];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t p0 = ((int64_t)blockIdx.x * Pw<K>::v + wib) * 32;
+    if (p0 >= A.nq) return;   // whole warp exits together
+    const int32_t pe = (int32_t)(p0 + 32 < (int64_t)A.nq ? p0 + 32 : (int64_t)A.nq);
+    const int32_t p = (int32_t)p0 + lane;
+    const bool active = p < pe;
+    const int32_t pq = active ? p : (int32_t)p0;
+    const int4 r = __ldg(A.qrecs + pq);
+    WarpSh<K>& S = sh[wib];
+    const Node<DIM>* nodes = static_cast<const Node<DIM>*>(A.nodes);
+
+    Lane<DIM, K> L;
+    L.q.c[0] = r.x; L.q.c[1] = r.y; L.q.c[2] = r.z;
+    L.q.id = EXT ? -1 : r.w;
+#pragma unroll
+    for (int t = 0; t < K; ++t) L.fa[t] = INFINITY;
+    L.U = active ? INT64_MAX : (int64_t)-1;   // an idle lane needs nothing, accepts nothing
+    L.cnt = 0;
+
+    int32_t lA, lB;
+    if (!EXT) {
+        lA = __ldg(A.qleaf + p0);
+        lB = __ldg(A.qleaf + pe - 1);
+    } else {
+        // bit-located leaves of Morton-sorted queries need not be monotone (a skipped
+        // bit can route a larger key left): take the packet's min..max, or just the min
+        // if that range is wide (any leaf range is a valid seed)
+        const int32_t ql = __ldg(A.qleaf + pq);
+        lA = ql;
+        lB = ql;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lA = min(lA, __shfl_xor_sync(0xffffffffu, lA, o));
+            lB = max(lB, __shfl_xor_sync(0xffffffffu, lB, o));
+        }
+        if (lB - lA > 8) lB = lA;
+    }
+    const int32_t ps_lo = __ldg(A.leaf_start + lA), ps_hi = __ldg(A.leaf_start + lB + 1);
+    scan_span<DIM, K>(A.recs, ps_lo, ps_hi, L, S, lane);
+
+    // C = the node whose subtree has been searched (-1: the single leaf lA)
+    int32_t C = -1, P;
+    Ref sub{kNoSub, 0};
+    if (lA == lB) {
+        P = __ldg(A.leaf_parent + lA);
+    } else {
+        int32_t x = __ldg(A.leaf_parent + lA);
+        while (__ldg(A.node_range + 2 * x + 1) < lB) x = __ldg(&nodes[x].parent);
+        C = x;
+        P = __ldg(&nodes[x].parent);
+        sub = Ref{x, 0};
+    }
+    while (true) {
+        if (sub.ref != kNoSub) joint_down<DIM, K>(A.recs, nodes, sub, ps_lo, ps_hi, L, S, lane);
+        if (P < 0) break;
+        ZD_STAT(ZS_ASCENTS, 1);
         const Node<DIM> nd = load_node<DIM>(nodes + P);
-        const bool isl = nd.left == C;
+        const bool isl = C >= 0 ? nd.left == C : P == lA;   // leaf l is the left child of node l
         int32_t cb[2 * DIM], sb[2 * DIM];
 #pragma unroll
         for (int a = 0; a < 2 * DIM; ++a) {
             cb[a] = isl ? nd.lbox[a] : nd.rbox[a];
             sb[a] = isl ? nd.rbox[a] : nd.lbox[a];
         }
-        if (stop_at<DIM>(q, cb, best.worst())) break;
-        search_down<DIM, K>(T, isl ? nd.right : nd.left, sb, q, best);
+        const int64_t w = L.U;
+        if (__all_sync(0xffffffffu, stop_at<DIM>(L.q, cb, w))) break;
+        sub = __any_sync(0xffffffffu, boxd2<DIM>(L.q, sb) <= w) ? (isl ? right_child<DIM>(nd) : left_child<DIM>(nd))
+                                                              : Ref{kNoSub, 0};
         C = P;
         P = nd.parent;
     }
-}
 
-template <int K>
-__device__ __forceinline__ void write_row(const KBest<K>& best, int k, int64_t row, int32_t* out_idx, int64_t* out_d2) {
-    int32_t* oi = out_idx + row * k;
-    int64_t* od = out_d2 + row * k;
+    // exact (d2, id) selection of the ~k surviving candidates
+    compact<DIM, K>(L, S, lane);
+#ifdef ZD_KNN_STATS
+    {
+        ZD_STAT(ZS_PACKETS, 1);
+        int sc = L.cnt, sm = L.cnt;
+        for (int o = 16; o > 0; o >>= 1) { sm = max(sm, __shfl_xor_sync(0xffffffffu, sm, o)); sc += __shfl_xor_sync(0xffffffffu, sc, o); }
+        ZD_STAT(ZS_SURV, sc);
+        ZD_STAT(ZS_SURV_MAX, sm);
+        ZD_STAT(ZS_QUERIES, __popc(__ballot_sync(0xffffffffu, active)));
+    }
+#endif
+    KBest<K> best;
+    best.init();
+    for (int e = 0; e < L.cnt; ++e) {
+        const int4 c = __ldg(A.recs + S.bp[e][lane]);
+        const int64_t d = dist2<DIM>(L.q, c);
+        if (best.accepts(d, c.w)) best.insert(d, c.w);
+    }
+    if (active) {
+        int64_t row;
+        if (EXT) row = r.w;
+        else row = A.row_of_id ? __ldg(A.row_of_id + r.w) : r.w;
+        int32_t* oi = A.out_idx + row * A.k;
+        int64_t* od = A.out_d2 + row * A.k;
 #pragma unroll
-    for (int s = 0; s < K; ++s) {
-        if (s < k) { oi[s] = best.i[s]; od[s] = best.d[s]; }
+        for (int s = 0; s < K; ++s) {
+            if (s < A.k) { oi[s] = best.i[s]; od[s] = best.d[s]; }
+        }
     }
 }
 
-template <int DIM, int K>
-__global__ void __launch_bounds__(128) knn_all_kernel(Tree T, const int32_t* __restrict__ pt_leaf, int32_t n, int k,
-                                                      const int32_t* __restrict__ row_of_id, int32_t* __restrict__ out_idx,
-                                                      int64_t* __restrict__ out_d2) {
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int4 r = __ldg(T.recs + i);
-    Query<DIM> q;
-    q.c[0] = r.x; q.c[1] = r.y; q.c[2] = r.z; q.id = r.w;
-    KBest<K> best;
-    best.init();
-    search_up<DIM, K>(T, __ldg(pt_leaf + i), q, best);
-    const int64_t row = row_of_id ? __ldg(row_of_id + r.w) : r.w;
-    write_row<K>(best, k, row, out_idx, out_d2);
-}
-
-template <int DIM, int K>
-__global__ void __launch_bounds__(128) knn_ext_kernel(Tree T, const int32_t* __restrict__ meta,
-                                                      const int32_t* __restrict__ queries, int32_t m, int k,
-                                                      int32_t* __restrict__ out_idx, int64_t* __restrict__ out_d2) {
-    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+// Bit-based leaf location: follow the query key's bit at each split.
+template <int DIM>
+__global__ void __launch_bounds__(256) locate_kernel(const uint64_t* __restrict__ qkeys, int32_t m,
+                                                     const Node<DIM>* __restrict__ nodes,
+                                                     const int32_t* __restrict__ split_bit,
+                                                     const int32_t* __restrict__ meta, int32_t* __restrict__ qleaf) {
+    const int32_t i = blockIdx.x * 256 + threadIdx.x;
     if (i >= m) return;
-    Query<DIM> q;
-    q.c[2] = 0;
-#pragma unroll
-    for (int a = 0; a < DIM; ++a) q.c[a] = __ldg(queries + (int64_t)i * DIM + a);
-    q.id = -1;
-    // bit-based leaf location: follow the query key's bit at each split
-    const uint64_t key = morton<DIM>(q.c[0], q.c[1], q.c[2]);
-    const Node<DIM>* nodes = static_cast<const Node<DIM>*>(T.nodes);
-    int32_t cur = __ldg(meta + 1);
+    const uint64_t key = __ldg(qkeys + i);
+    int32_t cur = __ldg(meta + 1);   // root: internal index, or ~0 for a single-leaf tree
+    int32_t leaf = 0;
     while (cur >= 0) {
-        const int4 tail = __ldg(reinterpret_cast<const int4*>(nodes + cur) + (sizeof(Node<DIM>) / 16 - 1));
-        cur = ((key >> tail.w) & 1u) ? tail.y : tail.x;   // (left, right, parent, split)
+        const bool right = (key >> __ldg(split_bit + cur)) & 1u;
+        const int32_t child = right ? __ldg(&nodes[cur].right) : __ldg(&nodes[cur].left);
+        if (child < 0) { leaf = right ? cur + 1 : cur; break; }   // leaf children of node i: i, i+1
+        cur = child;
     }
-    KBest<K> best;
-    best.init();
-    search_up<DIM, K>(T, ~cur, q, best);
-    write_row<K>(best, k, i, out_idx, out_d2);
+    qleaf[i] = leaf;
 }
 
-template <int DIM, int K>
-void launch_all(const KnnArgs& a, cudaStream_t st) {
-    Tree T{a.recs, a.leaf_start, a.leaf_parent, a.nodes};
-    const int grid = (int)((a.n + 127) / 128);
-    if (grid > 0) count_launch(1);
-    if (grid > 0)
-        knn_all_kernel<DIM, K><<<grid, 128, 0, st>>>(T, a.pt_leaf, (int32_t)a.n, a.k, a.row_of_id, a.out_idx, a.out_d2);
+PacketArgs packet_args(const KnnArgs& a) {
+    PacketArgs A{};
+    A.recs = a.recs; A.leaf_start = a.leaf_start; A.leaf_parent = a.leaf_parent;
+    A.nodes = a.nodes; A.node_range = a.node_range;
+    A.k = a.k; A.row_of_id = a.row_of_id; A.out_idx = a.out_idx; A.out_d2 = a.out_d2;
+    return A;
 }
 
-template <int DIM, int K>
-void launch_ext(const KnnArgs& a, const int32_t* queries, int64_t m, cudaStream_t st) {
-    Tree T{a.recs, a.leaf_start, a.leaf_parent, a.nodes};
-    const int grid = (int)((m + 127) / 128);
-    if (grid > 0) count_launch(1);
-    if (grid > 0) knn_ext_kernel<DIM, K><<<grid, 128, 0, st>>>(T, a.d_meta, queries, (int32_t)m, a.k, a.out_idx, a.out_d2);
+template <int DIM, int K, bool EXT>
+void launch_packets(const PacketArgs& A, cudaStream_t st) {
+    const int64_t warps = ((int64_t)A.nq + 31) / 32;
+    const int grid = (int)((warps + Pw<K>::v - 1) / Pw<K>::v);
+    if (grid <= 0) return;
+    count_launch(1);
+    knn_packet_kernel<DIM, K, EXT><<<grid, Pw<K>::v * 32, 0, st>>>(A);
 }
 
 #define ZD_K_CASES(X) X(1) X(4) X(8) X(10) X(16) X(32)
 
-template <int DIM>
-void all_dim(const KnnArgs& a, cudaStream_t st) {
-#define X(KK) if (a.k <= KK) { launch_all<DIM, KK>(a, st); return; }
-    ZD_K_CASES(X)
-#undef X
-}
-
-template <int DIM>
-void ext_dim(const KnnArgs& a, const int32_t* queries, int64_t m, cudaStream_t st) {
-#define X(KK) if (a.k <= KK) { launch_ext<DIM, KK>(a, queries, m, st); return; }
+template <int DIM, bool EXT>
+void dispatch(const PacketArgs& A, cudaStream_t st) {
+#define X(KK) if (A.k <= KK) { launch_packets<DIM, KK, EXT>(A, st); return; }
     ZD_K_CASES(X)
 #undef X
 }
@@ -270,13 +533,43 @@ void ext_dim(const KnnArgs& a, const int32_t* queries, int64_t m, cudaStream_t s
 
 int knn_kmax() { return 32; }
 
-void knn_all(const KnnArgs& a, cudaStream_t st) {
-    if (a.dim == 2) all_dim<2>(a, st); else all_dim<3>(a, st);
+int knn_stats(unsigned long long* out, int n, int reset) {
+#ifdef ZD_KNN_STATS
+    if (n > ZD_NSTATS) n = ZD_NSTATS;
+    if (cudaMemcpyFromSymbol(out, g_knn_stats, n * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    if (reset) {
+        unsigned long long z[ZD_NSTATS] = {};
+        cudaMemcpyToSymbol(g_knn_stats, z, sizeof(z));
+    }
+    return n;
+#else
+    (void)out; (void)n; (void)reset;
+    return -1;
+#endif
 }
 
-void knn_queries(const KnnArgs& a, const int32_t* queries, int64_t m, int* d_invalid, cudaStream_t st) {
-    (void)d_invalid;
-    if (a.dim == 2) ext_dim<2>(a, queries, m, st); else ext_dim<3>(a, queries, m, st);
+void knn_all(const KnnArgs& a, cudaStream_t st) {
+    PacketArgs A = packet_args(a);
+    A.qrecs = a.recs;
+    A.qleaf = a.pt_leaf;
+    A.nq = (int32_t)a.n;
+    if (a.dim == 2) dispatch<2, false>(A, st); else dispatch<3, false>(A, st);
+}
+
+void knn_queries(const KnnArgs& a, const uint64_t* qkeys, const int4* qrecs, int32_t* qleaf, int64_t m,
+                 cudaStream_t st) {
+    if (m <= 0) return;
+    const int grid = (int)((m + 255) / 256);
+    count_launch(1);
+    if (a.dim == 2)
+        locate_kernel<2><<<grid, 256, 0, st>>>(qkeys, (int32_t)m, (const Node<2>*)a.nodes, a.split_bit, a.d_meta, qleaf);
+    else
+        locate_kernel<3><<<grid, 256, 0, st>>>(qkeys, (int32_t)m, (const Node<3>*)a.nodes, a.split_bit, a.d_meta, qleaf);
+    PacketArgs A = packet_args(a);
+    A.qrecs = qrecs;
+    A.qleaf = qleaf;
+    A.nq = (int32_t)m;
+    if (a.dim == 2) dispatch<2, true>(A, st); else dispatch<3, true>(A, st);
 }
 
 }  // namespace zd

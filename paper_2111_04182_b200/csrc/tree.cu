@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(TT) compact_kernel(const uint8_t* __restrict__
                                                      uint32_t n, const uint32_t* __restrict__ block_off,
                                                      int32_t* __restrict__ split_bit, int32_t* __restrict__ leaf_start,
                                                      int32_t* __restrict__ pt_leaf, int32_t* __restrict__ meta,
-                                                     uint32_t* __restrict__ visit) {
+                                                     uint32_t* __restrict__ visit, int32_t* __restrict__ node_words,
+                                                     int nw) {
     __shared__ uint32_t s_warp[32];
     const int64_t base = (int64_t)blockIdx.x * TTILE + threadIdx.x * TPI;   // blocked per thread
     const int64_t npairs = (int64_t)n - 1;
@@ -102,6 +103,7 @@ __global__ void __launch_bounds__(TT) compact_kernel(const uint8_t* __restrict__
         if (f[i]) {
             split_bit[run] = delta_of(keys[p], keys[p + 1]);
             leaf_start[run + 1] = (int32_t)(p + 1);
+            node_words[(size_t)run * nw + nw - 1] = (int32_t)(p + 1);   // Node::mid
             visit[run] = 0u;   // bottom-up arrival counter of internal node `run`
             ++run;
         }
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__
             for (int a = 0; a < DIM; ++a) { bb[a] = min(bb[a], c[a]); bb[DIM + a] = max(bb[DIM + a], c[a]); }
         }
         if (nb == 0) { leaf_parent[0] = -1; continue; }
-        int32_t L = l, R = l, ref = ~l;
+        int32_t L = l, R = l, ref = -1;   // ref: internal node index, -1 while at the leaf
         while (true) {
             bool as_right;
             int32_t par;
@@ -149,9 +151,11 @@ __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__
             else if (__ldg(split_bit + L - 1) < __ldg(split_bit + R)) { par = L - 1; as_right = true; }
             else { par = R; as_right = false; }
             Node<DIM>* P = nodes + par;
-            if (as_right) { store_box<DIM>(P->rbox, bb); P->right = ref; range[2 * par + 1] = R; }
-            else { store_box<DIM>(P->lbox, bb); P->left = ref; range[2 * par] = L; }
-            if (ref < 0) leaf_parent[~ref] = par; else nodes[ref].parent = par;
+            // a leaf child is encoded by its point range: left = ~start, right = ~end
+            const int32_t cref = ref >= 0 ? ref : (as_right ? ~e : ~s);
+            if (as_right) { store_box<DIM>(P->rbox, bb); P->right = cref; range[2 * par + 1] = R; }
+            else { store_box<DIM>(P->lbox, bb); P->left = cref; range[2 * par] = L; }
+            if (ref < 0) leaf_parent[l] = par; else nodes[ref].parent = par;
             __threadfence();
             if (atomicAdd(visit + par, 1u) == 0) break;   // first child: the sibling finishes the parent
             __threadfence();
@@ -162,14 +166,37 @@ __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__
                 bb[DIM + a] = max(bb[DIM + a], __ldcg(sb + DIM + a));
             }
             if (as_right) L = __ldcg(range + 2 * par); else R = __ldcg(range + 2 * par + 1);
-            P->split = __ldg(split_bit + par);
             ref = par;
             if (L == 0 && R == nb) { P->parent = -1; meta[1] = par; break; }
         }
     }
 }
 
+template <int DIM>
+__global__ void __launch_bounds__(256) export_nodes_kernel(const Node<DIM>* __restrict__ nodes,
+                                                           const int32_t* __restrict__ split_bit, int64_t nb,
+                                                           int32_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (i >= nb) return;
+    const Node<DIM> nd = nodes[i];
+    int32_t* o = out + i * (4 * DIM + 4);
+#pragma unroll
+    for (int a = 0; a < 2 * DIM; ++a) { o[a] = nd.lbox[a]; o[2 * DIM + a] = nd.rbox[a]; }
+    o[4 * DIM] = nd.left >= 0 ? nd.left : ~(int32_t)i;             // left leaf child = leaf i
+    o[4 * DIM + 1] = nd.right >= 0 ? nd.right : ~(int32_t)(i + 1);  // right leaf child = leaf i+1
+    o[4 * DIM + 2] = nd.parent;
+    o[4 * DIM + 3] = split_bit[i];
+}
+
 }  // namespace
+
+void export_nodes(int dim, const void* nodes, const int32_t* split_bit, int64_t nb, int32_t* out, cudaStream_t st) {
+    if (nb <= 0) return;
+    const unsigned grid = (unsigned)((nb + 255) / 256);
+    count_launch(1);
+    if (dim == 2) export_nodes_kernel<2><<<grid, 256, 0, st>>>((const Node<2>*)nodes, split_bit, nb, out);
+    else export_nodes_kernel<3><<<grid, 256, 0, st>>>((const Node<3>*)nodes, split_bit, nb, out);
+}
 
 size_t tree_blocks(int64_t n) { return (size_t)std::max<int64_t>(1, (n - 1 + TTILE - 1) / TTILE); }
 
@@ -177,16 +204,19 @@ void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, 
                     cudaStream_t st, cudaEvent_t ev_mid) {
     const uint32_t un = (uint32_t)n;
     const size_t nblk = tree_blocks(n);
+    const int nw = dim == 2 ? (int)(sizeof(Node<2>) / 4) : (int)(sizeof(Node<3>) / 4);
     if (n <= 1) {
         // 0 or 1 point: a single (possibly empty) leaf; reuse the compaction kernel's
         // bookkeeping path with an empty pair range.
         cudaMemsetAsync(t.block_cnt, 0, 2 * sizeof(uint32_t), st);
-        compact_kernel<<<1, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta, t.visit);
+        compact_kernel<<<1, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta, t.visit,
+                                         (int32_t*)t.nodes, nw);
         count_launch(1);
     } else {
         flags_kernel<<<nblk, TT, 0, st>>>(keys, un, leaf_max, t.flags, t.block_cnt);
         scan_blocks_kernel<<<1, 1024, 0, st>>>(t.block_cnt, (uint32_t)nblk);
-        compact_kernel<<<nblk, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta, t.visit);
+        compact_kernel<<<nblk, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta,
+                                            t.visit, (int32_t*)t.nodes, nw);
         count_launch(3);
     }
     if (ev_mid) cudaEventRecord(ev_mid, st);

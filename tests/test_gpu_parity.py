@@ -91,6 +91,32 @@ def test_lattices_every_row(zd, oracle_mod):
             check_rows(gi, gd, bi, bd)
 
 
+def _far_corner_points(dim, seed):
+    """Fine lattices and near-ties at the top of the universe box, where fp32 cannot
+    represent 2D coordinates (ulp 64 at 2^30): exercises the fp32 prefilter's bound
+    (knn.cu filter_bound) against exact int64 distances and (d2, id) ties."""
+    B = 30 if dim == 2 else 21
+    top = (1 << B) - 1
+    rng = np.random.default_rng(seed)
+    g = zdgen.grid(12, dim).astype(np.int64) * 3            # lattice spacing 3
+    parts = [top - g,                                         # lattice in the far corner
+             top - rng.integers(0, 40, size=(3000, dim)),     # dense cloud, many ties
+             top - rng.integers(0, 1 << (B - 2), size=(3000, dim)),
+             rng.integers(0, 1 << B, size=(3000, dim)),
+             np.full((5, dim), top)]                          # coincident points
+    return np.ascontiguousarray(np.concatenate(parts).astype(np.int32))
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("k", [1, 10, 32])
+def test_knn_far_corner_ties(zd, oracle_mod, dim, k):
+    pts = _far_corner_points(dim, seed=dim * 100 + k)
+    t = zd.zd_build(dev(pts))
+    gi, gd = gpu_knn_all(t, k)
+    bi, bd = oracle_mod.brute_knn(pts, None, pts, np.arange(len(pts), dtype=np.int32), k)
+    check_rows(gi, gd, bi, bd)
+
+
 def test_c1_full_vs_brute_force(zd, oracle_mod):
     """Config C1 (65,536 2D uniform, seed 1): every row vs plain brute force."""
     pts = zdgen.config_points("C1")
