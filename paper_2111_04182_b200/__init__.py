@@ -47,11 +47,12 @@ class _Info(C.Structure):
 
 def load():
     """Load libzd.so (never rebuilt here).  ZD_LIB=stats selects the profiling variant
-    libzd_stats.so (work counters, zd_knn_stats)."""
+    libzd_stats.so (work counters, zd_knn_stats); ZD_LIB=<path>.so an experiment build."""
     global _lib
     if _lib is not None:
         return _lib
-    path = STATS_LIB_PATH if os.environ.get("ZD_LIB") == "stats" else LIB_PATH
+    sel = os.environ.get("ZD_LIB", "")
+    path = STATS_LIB_PATH if sel == "stats" else (Path(sel) if sel.endswith(".so") else LIB_PATH)
     if not path.exists():
         raise RuntimeError(f"{path.name} not built ({path}); run __graft_entry__.build()")
     L = C.CDLL(str(path))
@@ -227,7 +228,7 @@ class ZdTree:
 
 
 KNN_STATS = ("packets", "queries", "nodes", "pops", "ascents", "spans", "passes", "candidates", "hits",
-             "rounds", "compactions", "survivors", "survivors_max")
+             "rounds", "compactions", "survivors", "survivors_max", "cycles", "max_packet", "deferred") + tuple(f"hist{i}" for i in range(32))
 
 
 def zd_knn_stats(reset: bool = True) -> dict:

@@ -37,12 +37,13 @@ def stale(path: Path = LIB_PATH) -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build_lib(force: bool = False, verbose: bool = False, stats: bool = False) -> Path:
-    path = STATS_LIB_PATH if stats else LIB_PATH
+def build_lib(force: bool = False, verbose: bool = False, stats: bool = False, defines=(), out=None) -> Path:
+    """Build libzd.so (or, for experiments, a variant with extra -D defines at `out`)."""
+    path = Path(out) if out else (STATS_LIB_PATH if stats else LIB_PATH)
     if not force and not stale(path):
         return path
     tmp = path.with_name(f"{path.name}.tmp{os.getpid()}")
-    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DZD_KNN_STATS"] if stats else []),
+    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DZD_KNN_STATS"] if stats else []), *[f"-D{d}" for d in defines],
            *[str(CSRC / s) for s in SOURCES], "-o", str(tmp)]
     if verbose:
         print(" ".join(cmd))

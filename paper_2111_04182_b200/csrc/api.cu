@@ -436,7 +436,15 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
         ZD_CUDA(dalloc(&di, (size_t)m * k, h->st));
         ZD_CUDA(dalloc(&dd, (size_t)m * k, h->st));
     }
+    // scratch for packets deferred to the k-NN second pass (knn.cu): a count + a list
+    constexpr int kHardCap = 1 << 15;
+    int32_t* hard = nullptr;
+    ZD_CUDA(dalloc(&hard, kHardCap + 2, h->st));
+    ZD_CUDA(cudaMemsetAsync(hard, 0, sizeof(int32_t), h->st));
     KnnArgs a{};
+    a.hard_count = hard;
+    a.hard_list = hard + 2;
+    a.hard_cap = kHardCap;
     a.dim = h->dim; a.k = k; a.n = h->n;
     a.recs = h->recs; a.pt_leaf = h->tb.pt_leaf; a.leaf_start = h->tb.leaf_start;
     a.leaf_parent = h->tb.leaf_parent; a.nodes = h->tb.nodes; a.node_range = h->tb.range;
@@ -461,6 +469,7 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
         if (h->h_small[4]) {
             if (owned) cudaFreeAsync(owned, h->st);
             if (host_out) { dfree(di, h->st); dfree(dd, h->st); }
+            dfree(hard, h->st);
             return fail(ZD_ERANGE, "zd_knn: query outside the universe box");
         }
         // Morton-sort the queries (K1/K2; ids = query index), locate their leaves by
@@ -481,6 +490,7 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
         dfree(qr, h->st);
         dfree(ql, h->st);
     }
+    dfree(hard, h->st);
     if (host_out) {
         ZD_CUDA(cudaMemcpyAsync(out_idx, di, (size_t)m * k * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
         ZD_CUDA(cudaMemcpyAsync(out_dist2, dd, (size_t)m * k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->st));

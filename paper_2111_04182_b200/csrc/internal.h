@@ -64,11 +64,14 @@ struct KnnArgs {
     const int32_t* row_of_id;    // NULL: row = id
     int32_t* out_idx;
     int64_t* out_d2;
+    int32_t* hard_list;          // [hard_cap] scratch for deferred packets (NULL: none)
+    int32_t* hard_count;         // zeroed by the caller
+    int hard_cap;
 };
 int knn_kmax();
 // Work counters of the packet k-NN kernel (only in a -DZD_KNN_STATS build).
 enum { ZS_PACKETS = 0, ZS_QUERIES, ZS_NODES, ZS_POPS, ZS_ASCENTS, ZS_SPANS, ZS_PASSES, ZS_CAND, ZS_HITS,
-       ZS_ROUNDS, ZS_COMPACT, ZS_SURV, ZS_SURV_MAX, ZD_NSTATS };
+       ZS_ROUNDS, ZS_COMPACT, ZS_SURV, ZS_SURV_MAX, ZS_CYCLES, ZS_MAXPKT, ZS_DEFERRED, ZS_HIST0, ZD_NSTATS = ZS_HIST0 + 32 };
 int knn_stats(unsigned long long* out, int n, int reset);
 void knn_all(const KnnArgs& a, cudaStream_t st);
 // External queries, already Morton-sorted (qkeys, qrecs with w = query index):

@@ -135,6 +135,9 @@ template <int K>
 struct Pw {
     static constexpr int v = K <= 16 ? 4 : 2;   // warps per block (shared memory grows with K)
 };
+#ifndef ZD_MINB
+#define ZD_MINB 4         // min resident blocks per SM for K <= 10 (register budget)
+#endif
 constexpr int CH = 16;                   // candidates tested per uniform pass
 constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
 
@@ -364,6 +367,7 @@ struct PacketArgs {
     const int32_t* leaf_parent;
     const void* nodes;
     const int32_t* node_range;
+    const int32_t* split_bit;  // per internal node (in-order)
     const int4* qrecs;         // queries in Morton order: (x, y, z|0, id or query index)
     const int32_t* qleaf;      // leaf of each query
     int32_t nq;
@@ -371,23 +375,32 @@ struct PacketArgs {
     const int32_t* row_of_id;  // all-points: row of an id (NULL: row = id)
     int32_t* out_idx;
     int64_t* out_d2;
+    int32_t* hard_list;        // packets deferred to the second pass (NULL: never defer)
+    int32_t* hard_count;
+    int hard_cap;
+    int hard_mode;             // 0: packets; 1: second pass over the deferred packets' queries
 };
+
+#ifndef ZD_INCOHERENT
+#define ZD_INCOHERENT 1024.0f   // defer a packet if its extent^2 > this * median bound
+#endif
+
 
 // EXT = false: all-points (queries are the tree's own points; self excluded by id,
 // row = row_of_id[id]).  EXT = true: external queries (nothing excluded, row = query
 // index carried in the record's w).
+// Search the queries at Morton positions [p0, pe) (pe - p0 <= 32) as one packet.
+// Returns false (writing nothing) if the packet was deferred to the second pass.
 template <int DIM, int K, bool EXT>
-__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? 4 : 2)) knn_packet_kernel(PacketArgs A) {
-    __shared__ WarpSh<K> sh[Pw<K>::v];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int64_t p0 = ((int64_t)blockIdx.x * Pw<K>::v + wib) * 32;
-    if (p0 >= A.nq) return;   // whole warp exits together
-    const int32_t pe = (int32_t)(p0 + 32 < (int64_t)A.nq ? p0 + 32 : (int64_t)A.nq);
-    const int32_t p = (int32_t)p0 + lane;
+__device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, int32_t pe, int64_t pk, bool can_defer,
+                                              WarpSh<K>& S, int lane) {
+    const int32_t p = p0 + lane;
     const bool active = p < pe;
-    const int32_t pq = active ? p : (int32_t)p0;
+    const int32_t pq = active ? p : p0;
     const int4 r = __ldg(A.qrecs + pq);
-    WarpSh<K>& S = sh[wib];
+#ifdef ZD_KNN_STATS
+    const long long t_start = clock64();
+#endif
     const Node<DIM>* nodes = static_cast<const Node<DIM>*>(A.nodes);
 
     Lane<DIM, K> L;
@@ -419,14 +432,71 @@ __global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? 4 : 2)) knn_packet_k
     const int32_t ps_lo = __ldg(A.leaf_start + lA), ps_hi = __ldg(A.leaf_start + lB + 1);
     scan_span<DIM, K>(A.recs, ps_lo, ps_hi, L, S, lane);
 
+    if (can_defer) {
+        // A packet whose queries are far apart compared with their neighbour distances
+        // (32 Morton-consecutive points straddling a large Morton-cell boundary) would
+        // make one warp search several distant regions jointly; it is deferred to a
+        // second pass that searches its queries one per warp.
+        float ext2 = 0.f;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            int mn = L.q.c[a], mx = L.q.c[a];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            }
+            const float e = (float)(mx - mn);
+            ext2 = fmaxf(ext2, e * e);
+        }
+        const bool fin = active && L.U != INT64_MAX;
+        const int nfin = __popc(__ballot_sync(0xffffffffu, fin));
+        const int nact = __popc(__ballot_sync(0xffffffffu, active));
+        // median over the active lanes of log2(bound + 1) (bitonic sort across the warp;
+        // idle lanes sort last)
+        float v = active ? (fin ? __log2f((float)L.U + 1.0f) : 1e30f) : INFINITY;
+#pragma unroll
+        for (int kk = 2; kk <= 32; kk <<= 1) {
+#pragma unroll
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                const float o = __shfl_xor_sync(0xffffffffu, v, j);
+                const bool up = (lane & kk) == 0, lower = (lane & j) == 0;
+                v = (lower == up) ? fminf(v, o) : fmaxf(v, o);
+            }
+        }
+        const float med = __shfl_sync(0xffffffffu, v, nact >> 1);
+        if (nfin == nact && ext2 > ZD_INCOHERENT * exp2f(med)) {
+            int slot = 0;
+            if (lane == 0) slot = atomicAdd(A.hard_count, 1);
+            slot = __shfl_sync(0xffffffffu, slot, 0);
+            if (slot < A.hard_cap) {
+                if (lane == 0) A.hard_list[slot] = (int32_t)pk;
+                ZD_STAT(ZS_DEFERRED, 1);
+                return false;
+            }
+        }
+    }
+
     // C = the node whose subtree has been searched (-1: the single leaf lA)
     int32_t C = -1, P;
     Ref sub{kNoSub, 0};
     if (lA == lB) {
         P = __ldg(A.leaf_parent + lA);
     } else {
-        int32_t x = __ldg(A.leaf_parent + lA);
-        while (__ldg(A.node_range + 2 * x + 1) < lB) x = __ldg(&nodes[x].parent);
+        // lowest common ancestor of leaves lA < lB = the separator node in [lA, lB)
+        // with the highest split bit (the canonical tree is the Cartesian tree of the
+        // split bits; two equal bits in a range always have a higher one between them)
+        int32_t bb = -2, x = lA;
+        for (int32_t i0 = lA; i0 < lB; i0 += 32) {
+            const int32_t i = i0 + lane;
+            const int32_t v = i < lB ? __ldg(A.split_bit + i) : -2;
+            if (v > bb) { bb = v; x = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int32_t ob = __shfl_xor_sync(0xffffffffu, bb, o), ox = __shfl_xor_sync(0xffffffffu, x, o);
+            if (ob > bb) { bb = ob; x = ox; }
+        }
         C = x;
         P = __ldg(&nodes[x].parent);
         sub = Ref{x, 0};
@@ -460,7 +530,12 @@ __global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? 4 : 2)) knn_packet_k
         for (int o = 16; o > 0; o >>= 1) { sm = max(sm, __shfl_xor_sync(0xffffffffu, sm, o)); sc += __shfl_xor_sync(0xffffffffu, sc, o); }
         ZD_STAT(ZS_SURV, sc);
         ZD_STAT(ZS_SURV_MAX, sm);
-        ZD_STAT(ZS_QUERIES, __popc(__ballot_sync(0xffffffffu, active)));
+        const int nact = __popc(__ballot_sync(0xffffffffu, active));
+        ZD_STAT(ZS_QUERIES, nact);
+        const long long dt = clock64() - t_start;
+        ZD_STAT(ZS_CYCLES, dt);
+        ZD_STAT(ZS_HIST0 + min(31, 63 - __clzll(dt | 1)), 1);
+        if (lane == 0) atomicMax(&g_knn_stats[ZS_MAXPKT], ((unsigned long long)dt << 24) | (unsigned long long)(p0 >> 5));
     }
 #endif
     KBest<K> best;
@@ -479,6 +554,30 @@ __global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? 4 : 2)) knn_packet_k
 #pragma unroll
         for (int s = 0; s < K; ++s) {
             if (s < A.k) { oi[s] = best.i[s]; od[s] = best.d[s]; }
+        }
+    }
+    return true;
+}
+
+template <int DIM, int K, bool EXT>
+__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? ZD_MINB : 2)) knn_packet_kernel(PacketArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpSh<K>* sh = reinterpret_cast<WarpSh<K>*>(smem_raw);   // Pw<K>::v warps
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSh<K>& S = sh[wib];
+    const int64_t gw = (int64_t)blockIdx.x * Pw<K>::v + wib;
+    if (!A.hard_mode) {
+        const int64_t p0 = gw * 32;
+        if (p0 >= A.nq) return;   // whole warp exits together
+        const int32_t pe = (int32_t)(p0 + 32 < (int64_t)A.nq ? p0 + 32 : (int64_t)A.nq);
+        search_packet<DIM, K, EXT>(A, (int32_t)p0, pe, gw, A.hard_list != nullptr, S, lane);
+    } else {
+        // second pass: the deferred packets' queries, one per warp (grid-stride)
+        const int64_t cnt = min(*A.hard_count, A.hard_cap);
+        const int64_t total = (int64_t)gridDim.x * Pw<K>::v;
+        for (int64_t t = gw; t < cnt * 32; t += total) {
+            const int64_t pos = (int64_t)__ldg(A.hard_list + (t >> 5)) * 32 + (t & 31);
+            if (pos < A.nq) search_packet<DIM, K, EXT>(A, (int32_t)pos, (int32_t)pos + 1, 0, false, S, lane);
         }
     }
 }
@@ -506,8 +605,9 @@ __global__ void __launch_bounds__(256) locate_kernel(const uint64_t* __restrict_
 PacketArgs packet_args(const KnnArgs& a) {
     PacketArgs A{};
     A.recs = a.recs; A.leaf_start = a.leaf_start; A.leaf_parent = a.leaf_parent;
-    A.nodes = a.nodes; A.node_range = a.node_range;
+    A.nodes = a.nodes; A.node_range = a.node_range; A.split_bit = a.split_bit;
     A.k = a.k; A.row_of_id = a.row_of_id; A.out_idx = a.out_idx; A.out_d2 = a.out_d2;
+    A.hard_list = a.hard_list; A.hard_count = a.hard_count; A.hard_cap = a.hard_cap; A.hard_mode = 0;
     return A;
 }
 
@@ -516,8 +616,23 @@ void launch_packets(const PacketArgs& A, cudaStream_t st) {
     const int64_t warps = ((int64_t)A.nq + 31) / 32;
     const int grid = (int)((warps + Pw<K>::v - 1) / Pw<K>::v);
     if (grid <= 0) return;
+    const size_t smem = sizeof(WarpSh<K>) * Pw<K>::v;
+    static bool attr_set = false;   // per template instance
+    if (!attr_set) {
+        cudaFuncSetAttribute(knn_packet_kernel<DIM, K, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
     count_launch(1);
-    knn_packet_kernel<DIM, K, EXT><<<grid, Pw<K>::v * 32, 0, st>>>(A);
+    knn_packet_kernel<DIM, K, EXT><<<grid, Pw<K>::v * 32, smem, st>>>(A);
+    if (A.hard_list) {
+        PacketArgs H = A;
+        H.hard_mode = 1;
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        count_launch(1);
+        knn_packet_kernel<DIM, K, EXT><<<sms * 4, Pw<K>::v * 32, smem, st>>>(H);
+    }
 }
 
 #define ZD_K_CASES(X) X(1) X(4) X(8) X(10) X(16) X(32)

@@ -31,8 +31,15 @@ def main():
         torch.cuda.synchronize()
         s = zd.zd_knn_stats(reset=True)
         p, q = s["packets"], s["queries"]
-        out = {"config": name, "k": args.k, **s,
-               "per_packet": {k: round(v / p, 2) for k, v in s.items() if k not in ("packets", "queries")},
+        hist = {i: s.pop(f"hist{i}") for i in range(32) if s.get(f"hist{i}")}
+        cyc = s["cycles"]
+        mp = s.pop("max_packet")
+        s["slowest_packet"] = {"packet": mp & 0xFFFFFF, "cycles": mp >> 24}
+        # share of all packet-cycles spent in packets of 2^i .. 2^(i+1) cycles
+        out = {"config": name, "k": args.k, "cycle_hist_log2": hist,
+               "mean_cycles_per_packet": round(cyc / s["packets"]), **s,
+               "per_packet": {k: round(v / p, 2) for k, v in s.items()
+                              if k not in ("packets", "queries", "slowest_packet")},
                "per_query": {"candidates_per_lane": round(s["candidates"] / p, 1), "hits": round(s["hits"] / q, 2),
                              "survivors": round(s["survivors"] / q, 2)}}
         print(json.dumps(out), flush=True)
