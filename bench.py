@@ -240,7 +240,7 @@ def alu_ops_per_query(per_q: dict) -> float:
 
 def load_traffic():
     """Per-launch DRAM bytes of the k-NN kernel from the committed ncu capture, if any."""
-    for p in sorted((ROOT / "profiles").glob("ncu_knn_*.json"), reverse=True):
+    for p in sorted((ROOT / "profiles").glob("*ncu_knn*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
             return d.get("dram_bytes_per_launch"), p.name

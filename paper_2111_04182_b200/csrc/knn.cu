@@ -136,14 +136,21 @@ struct Pw {
     static constexpr int v = K <= 16 ? 4 : 2;   // warps per block (shared memory grows with K)
 };
 #ifndef ZD_MINB
-#define ZD_MINB 4         // min resident blocks per SM for K <= 10 (register budget)
+#define ZD_MINB 6         // min resident blocks per SM for K <= 10 (register budget)
 #endif
 constexpr int CH = 16;                   // candidates tested per uniform pass
 constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
+#ifndef ZD_STK
+#define ZD_STK kMaxDepth
+#endif
+constexpr int kStk = ZD_STK;             // per-warp stack entries (>= tree height; 64 = key bits + 1)
 
+#ifndef ZD_CAP_MIN
+#define ZD_CAP_MIN 26
+#endif
 template <int K>
 struct Cap {
-    static constexpr int v = (K + CH > 32) ? K + CH : 32;   // buffered candidates per lane
+    static constexpr int v = (K + CH > ZD_CAP_MIN) ? K + CH : ZD_CAP_MIN;   // buffered candidates per lane
 };
 
 // A child reference in traversal form: ref >= 0 internal node; ref < 0 a leaf with
@@ -168,7 +175,7 @@ struct WarpSh {
     int4 c[32];                          // staged candidates (x, y, z|0, id)
     int32_t bp[Cap<K>::v][32];           // per-lane buffered positions; column = lane
     float bf[Cap<K>::v][32];             //   ... and their d2 rounded up to fp32
-    StkEntry stk[kMaxDepth];
+    StkEntry stk[kStk];
 };
 
 template <int DIM, int K>
