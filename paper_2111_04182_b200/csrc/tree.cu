@@ -24,6 +24,7 @@
 //    the second merges both boxes and continues (atomic arrival counter).  Linear
 //    work, one pass, no recursion.
 #include <algorithm>
+#include <cuda/atomic>
 
 #include "common.cuh"
 #include "internal.h"
@@ -136,8 +137,8 @@ __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__
         for (int a = 0; a < DIM; ++a) { bb[a] = INT32_MAX; bb[DIM + a] = INT32_MIN; }
         const int32_t s = leaf_start[l], e = leaf_start[l + 1];
         for (int32_t j = s; j < e; ++j) {
-            int4 r = __ldg(recs + j);
-            int c[3] = {r.x, r.y, r.z};
+            const int4 r = __ldg(recs + j);
+            const int c[3] = {r.x, r.y, r.z};
 #pragma unroll
             for (int a = 0; a < DIM; ++a) { bb[a] = min(bb[a], c[a]); bb[DIM + a] = max(bb[DIM + a], c[a]); }
         }
@@ -156,9 +157,12 @@ __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__
             if (as_right) { store_box<DIM>(P->rbox, bb); P->right = cref; range[2 * par + 1] = R; }
             else { store_box<DIM>(P->lbox, bb); P->left = cref; range[2 * par] = L; }
             if (ref < 0) leaf_parent[l] = par; else nodes[ref].parent = par;
-            __threadfence();
-            if (atomicAdd(visit + par, 1u) == 0) break;   // first child: the sibling finishes the parent
-            __threadfence();
+            // release: our box/ref/range writes are visible before the count; acquire:
+            // the second arriver sees its sibling's (one MEMBAR + one L1 invalidate,
+            // instead of two sequentially consistent fences)
+            const uint32_t arrived =
+                cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(visit[par]).fetch_add(1u, cuda::memory_order_acq_rel);
+            if (arrived == 0) break;   // first child: the sibling finishes the parent
             const int32_t* sb = as_right ? P->lbox : P->rbox;
 #pragma unroll
             for (int a = 0; a < DIM; ++a) {
@@ -223,7 +227,9 @@ void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int grid = (int)std::min<int64_t>((int64_t)sms * 16, std::max<int64_t>(1, (n / 8 + 127) / 128));
+    // about one thread per leaf (leaves <= n / 4 unless leaf_max is tiny: grid-stride)
+    (void)sms;
+    int grid = (int)std::max<int64_t>(1, (n / 4 + 127) / 128);
     count_launch(1);
     if (dim == 2)
         bottom_up_kernel<2><<<grid, 128, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<2>*)t.nodes,

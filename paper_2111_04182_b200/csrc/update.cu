@@ -32,40 +32,63 @@ __global__ void __launch_bounds__(256) validate_kernel(const int32_t* __restrict
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(invalid, 1);
 }
 
-constexpr int MT = 128;
+constexpr int MT = 256;
 constexpr int MI = 8;
+constexpr int MTILE = MT * MI;   // outputs per block
 
-// Merge path: thread t produces outputs [t*MI, t*MI+MI).  A (resident points) wins ties.
-__global__ void __launch_bounds__(MT) merge_kernel(const uint64_t* __restrict__ ka, const int4* __restrict__ ra, int64_t n,
-                                                   const uint64_t* __restrict__ kb, const int4* __restrict__ rb, int64_t m,
-                                                   uint64_t* __restrict__ ko, int4* __restrict__ ro) {
-    const int64_t diag = ((int64_t)blockIdx.x * MT + threadIdx.x) * MI;
-    const int64_t tot = n + m;
-    if (diag >= tot) return;
+// merge path: number of A elements among the first `diag` outputs (A wins ties)
+__device__ __forceinline__ int64_t merge_split(const uint64_t* __restrict__ ka, int64_t n, const uint64_t* __restrict__ kb,
+                                               int64_t m, int64_t diag) {
     int64_t lo = max((int64_t)0, diag - m), hi = min(diag, n);
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if (__ldg(ka + mid) <= __ldg(kb + diag - 1 - mid)) lo = mid + 1; else hi = mid;
     }
-    int64_t ia = lo, ib = diag - lo;
-    uint64_t a = ia < n ? __ldg(ka + ia) : ~0ull;
-    uint64_t b = ib < m ? __ldg(kb + ib) : ~0ull;
-#pragma unroll
-    for (int t = 0; t < MI; ++t) {
-        const int64_t o = diag + t;
-        if (o >= tot) break;
-        const bool take_a = ib >= m || (ia < n && a <= b);
-        if (take_a) {
-            ko[o] = a;
-            ro[o] = __ldg(ra + ia);
-            ++ia;
-            a = ia < n ? __ldg(ka + ia) : ~0ull;
-        } else {
-            ko[o] = b;
-            ro[o] = __ldg(rb + ib);
-            ++ib;
-            b = ib < m ? __ldg(kb + ib) : ~0ull;
+    return lo;
+}
+
+// Block-tiled merge path: a block owns MTILE consecutive outputs; it stages the two
+// input key runs in shared memory, each thread merges MI outputs there and records
+// their sources, and the block then writes keys and records coalesced.
+__global__ void __launch_bounds__(MT) merge_kernel(const uint64_t* __restrict__ ka, const int4* __restrict__ ra, int64_t n,
+                                                   const uint64_t* __restrict__ kb, const int4* __restrict__ rb, int64_t m,
+                                                   uint64_t* __restrict__ ko, int4* __restrict__ ro) {
+    __shared__ uint64_t s_key[MTILE];
+    __shared__ int32_t s_src[MTILE];   // >= 0: A offset in the tile; < 0: ~B offset
+    __shared__ int64_t s_split[2];
+    const int64_t tot = n + m;
+    const int64_t d0 = (int64_t)blockIdx.x * MTILE;
+    const int64_t d1 = min(d0 + MTILE, tot);
+    if (threadIdx.x < 2) s_split[threadIdx.x] = merge_split(ka, n, kb, m, threadIdx.x ? d1 : d0);
+    __syncthreads();
+    const int64_t a0 = s_split[0], a1 = s_split[1];
+    const int64_t b0 = d0 - a0, b1 = d1 - a1;
+    const int na = (int)(a1 - a0), nb = (int)(b1 - b0);
+    for (int i = threadIdx.x; i < na + nb; i += MT)
+        s_key[i] = i < na ? __ldg(ka + a0 + i) : __ldg(kb + b0 + (i - na));
+    __syncthreads();
+    // this thread's outputs [t0, t0 + MI) within the tile
+    const int t0 = threadIdx.x * MI;
+    if (t0 < na + nb) {
+        int lo = max(0, t0 - nb), hi = min(t0, na);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_key[mid] <= s_key[na + t0 - 1 - mid]) lo = mid + 1; else hi = mid;
         }
+        int ia = lo, ib = t0 - lo;
+#pragma unroll
+        for (int t = 0; t < MI; ++t) {
+            const int o = t0 + t;
+            if (o >= na + nb) break;
+            const bool take_a = ib >= nb || (ia < na && s_key[ia] <= s_key[na + ib]);
+            s_src[o] = take_a ? ia++ : ~(ib++);
+        }
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < na + nb; o += MT) {
+        const int sidx = s_src[o];
+        ko[d0 + o] = sidx >= 0 ? s_key[sidx] : s_key[na + ~sidx];
+        ro[d0 + o] = sidx >= 0 ? __ldg(ra + a0 + sidx) : __ldg(rb + b0 + ~sidx);
     }
 }
 
@@ -119,29 +142,54 @@ __global__ void __launch_bounds__(CT) compact_count_kernel(const uint32_t* __res
     if (threadIdx.x == 0) block_cnt[blockIdx.x] = tot;
 }
 
+// Stable compaction of one CTILE tile: element (j, t) = base + j*CT + t is read
+// coalesced; its output rank = kept elements before it in (j, warp, lane) order, from
+// per-(j, warp) ballot counts scanned by one warp.
 __global__ void __launch_bounds__(CT) compact_write_kernel(const uint32_t* __restrict__ alive, const uint64_t* __restrict__ ki,
                                                            const int4* __restrict__ ri, int64_t n,
                                                            const uint32_t* __restrict__ block_off,
                                                            uint64_t* __restrict__ ko, int4* __restrict__ ro) {
-    __shared__ uint32_t s_warp[32];
-    const int64_t base = (int64_t)blockIdx.x * CTILE + (int64_t)threadIdx.x * CPI;   // blocked: keeps order
+    constexpr int NW = CT / 32;
+    __shared__ uint32_t s_cnt[CPI * NW];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t base = (int64_t)blockIdx.x * CTILE + threadIdx.x;
     int4 r[CPI];
-    uint32_t keep = 0, c = 0;
+    uint32_t bal[CPI];
 #pragma unroll
-    for (int t = 0; t < CPI; ++t) {
-        const int64_t i = base + t;
+    for (int j = 0; j < CPI; ++j) {
+        const int64_t i = base + (int64_t)j * CT;
+        bool keep = false;
         if (i < n) {
-            r[t] = __ldg(ri + i);
-            if (is_alive(alive, r[t].w)) { keep |= 1u << t; ++c; }
+            r[j] = __ldg(ri + i);
+            keep = is_alive(alive, r[j].w);
+        }
+        bal[j] = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_cnt[j * NW + w] = __popc(bal[j]);
+    }
+    __syncthreads();
+    if (w == 0) {   // exclusive scan of the CPI*NW counts (j-major, then warp)
+        uint32_t carry = 0;
+        for (int c0 = 0; c0 < CPI * NW; c0 += 32) {
+            const uint32_t v = c0 + lane < CPI * NW ? s_cnt[c0 + lane] : 0u;
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (c0 + lane < CPI * NW) s_cnt[c0 + lane] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
     }
-    uint32_t o = block_off[blockIdx.x] + block_exclusive_scan<CT>(c, s_warp, nullptr);
+    __syncthreads();
+    const uint32_t off = block_off[blockIdx.x];
+    const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int t = 0; t < CPI; ++t) {
-        if (keep & (1u << t)) {
-            ko[o] = __ldg(ki + base + t);
-            ro[o] = r[t];
-            ++o;
+    for (int j = 0; j < CPI; ++j) {
+        if ((bal[j] >> lane) & 1u) {
+            const uint32_t o = off + s_cnt[j * NW + w] + __popc(bal[j] & lt);
+            ko[o] = __ldg(ki + base + (int64_t)j * CT);
+            ro[o] = r[j];
         }
     }
 }
@@ -158,21 +206,28 @@ __global__ void __launch_bounds__(RT) rank_count_kernel(const uint32_t* __restri
     if (threadIdx.x == 0) block_cnt[blockIdx.x] = tot;
 }
 
+// One block = the 256 alive words (8192 ids) of rank_count_kernel's block; ids are
+// then visited one per thread (coalesced row_of_id writes).
 __global__ void __launch_bounds__(RT) rank_write_kernel(const uint32_t* __restrict__ alive, int64_t words, int64_t id_cap,
                                                         const uint32_t* __restrict__ block_off,
                                                         int32_t* __restrict__ row_of_id, int32_t* __restrict__ live_ids) {
     __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_bits[RT], s_pre[RT];
     const int64_t w = (int64_t)blockIdx.x * RT + threadIdx.x;
     const uint32_t bits = w < words ? __ldg(alive + w) : 0u;
-    uint32_t r = block_off[blockIdx.x] + block_exclusive_scan<RT>(__popc(bits), s_warp, nullptr);
-    if (w >= words) return;
-    for (int b = 0; b < 32; ++b) {
-        const int64_t id = (w << 5) + b;
+    s_bits[threadIdx.x] = bits;
+    s_pre[threadIdx.x] = block_off[blockIdx.x] + block_exclusive_scan<RT>(__popc(bits), s_warp, nullptr);
+    __syncthreads();
+    const int64_t id0 = (int64_t)blockIdx.x * RT * 32;
+    for (int t = threadIdx.x; t < RT * 32; t += RT) {
+        const int64_t id = id0 + t;
         if (id >= id_cap) break;
-        if ((bits >> b) & 1u) {
+        const uint32_t b = s_bits[t >> 5];
+        const int bit = t & 31;
+        if ((b >> bit) & 1u) {
+            const uint32_t r = s_pre[t >> 5] + __popc(b & ((1u << bit) - 1u));
             row_of_id[id] = (int32_t)r;
             live_ids[r] = (int32_t)id;
-            ++r;
         } else {
             row_of_id[id] = -1;
         }
@@ -194,8 +249,7 @@ void merge_sorted(const uint64_t* ka, const int4* ra, int64_t n, const uint64_t*
                   uint64_t* ko, int4* ro, cudaStream_t st) {
     const int64_t tot = n + m;
     if (tot <= 0) return;
-    const int64_t threads = (tot + MI - 1) / MI;
-    merge_kernel<<<(unsigned)((threads + MT - 1) / MT), MT, 0, st>>>(ka, ra, n, kb, rb, m, ko, ro);
+    merge_kernel<<<(unsigned)((tot + MTILE - 1) / MTILE), MT, 0, st>>>(ka, ra, n, kb, rb, m, ko, ro);
     count_launch(1);
 }
 
