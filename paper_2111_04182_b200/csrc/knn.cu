@@ -131,9 +131,16 @@ __device__ __forceinline__ Node<DIM> load_node(const Node<DIM>* p) {
     return r;
 }
 
+#ifndef ZD_PW
+#define ZD_PW 4
+#endif
+#ifndef ZD_UNROLL
+#define ZD_UNROLL 4
+#endif
+constexpr int kUnroll = ZD_UNROLL;   // uniform candidate loop unrolling
 template <int K>
 struct Pw {
-    static constexpr int v = K <= 16 ? 4 : 2;   // warps per block (shared memory grows with K)
+    static constexpr int v = K <= 16 ? ZD_PW : 2;   // warps per block (shared memory grows with K)
 };
 #ifndef ZD_MINB
 #define ZD_MINB 6         // min resident blocks per SM for K <= 10 (register budget)
@@ -176,6 +183,7 @@ struct WarpSh {
     int32_t bp[Cap<K>::v][32];           // per-lane buffered positions; column = lane
     float bf[Cap<K>::v][32];             //   ... and their d2 rounded up to fp32
     StkEntry stk[kStk];
+    int4 nbuf[2][4];                     // lookahead: the current node's children (cp.async)
 };
 
 template <int DIM, int K>
@@ -252,7 +260,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
             }
             const int64_t U = L.U;
             uint32_t hit = 0;
-#pragma unroll 4
+#pragma unroll kUnroll
             for (int j = 0; j < cnt; ++j) {
                 const int4 c = S.c[h0 + j];
                 const bool h = dist2<DIM>(L.q, c) <= U && c.w != L.q.id;   // self excluded by id
@@ -301,6 +309,16 @@ __device__ __forceinline__ void scan_leaves(const int4* __restrict__ recs, int32
     if (a < b) scan_span<DIM, K>(recs, a, b, L, S, lane);
 }
 
+#ifndef ZD_LOOKAHEAD
+#define ZD_LOOKAHEAD 0
+#endif
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int DIM>
 __device__ __forceinline__ void unpack_box(const StkEntry& e, int32_t (&bx)[2 * DIM]) {
     const int w[6] = {e.a.y, e.a.z, e.a.w, e.b.x, e.b.y, e.b.z};
@@ -312,14 +330,36 @@ __device__ __forceinline__ void unpack_box(const StkEntry& e, int32_t (&bx)[2 * 
 template <int DIM, int K>
 __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const Node<DIM>* __restrict__ nodes, Ref cur,
                                            int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
+    constexpr int NW = (int)(sizeof(Node<DIM>) / 16);
     int sp = 0;
+    int nd_side = -1;   // >= 0: cur's node is (arriving) in S.nbuf[nd_side]
     while (true) {
         bool descend = false;
         if (cur.ref < 0) {
             scan_leaves<DIM, K>(recs, ~cur.ref, cur.end, cur.end, ps_lo, ps_hi, L, S, lane);
         } else {
             ZD_STAT(ZS_NODES, 1);
-            const Node<DIM> nd = load_node<DIM>(nodes + cur.ref);
+            Node<DIM> nd;
+            if (ZD_LOOKAHEAD && nd_side >= 0) {
+                cp_async_wait();
+                __syncwarp();
+                int4* d = reinterpret_cast<int4*>(&nd);
+#pragma unroll
+                for (int t = 0; t < NW; ++t) d[t] = S.nbuf[nd_side][t];
+            } else {
+                nd = load_node<DIM>(nodes + cur.ref);
+            }
+            nd_side = -1;
+            if (ZD_LOOKAHEAD) {
+                // copy the internal children's nodes to shared memory while testing boxes
+                cp_async_wait();
+                __syncwarp();
+                if (nd.left >= 0 && lane < NW)
+                    cp_async16(&S.nbuf[0][lane], reinterpret_cast<const int4*>(nodes + nd.left) + lane);
+                if (nd.right >= 0 && lane >= 4 && lane < 4 + NW)
+                    cp_async16(&S.nbuf[1][lane - 4], reinterpret_cast<const int4*>(nodes + nd.right) + (lane - 4));
+                cp_async_commit();
+            }
             const int64_t w = L.U;
             const int64_t dl = boxd2<DIM>(L.q, nd.lbox), dr = boxd2<DIM>(L.q, nd.rbox);
             const bool nl = __any_sync(0xffffffffu, dl <= w), nr = __any_sync(0xffffffffu, dr <= w);
@@ -342,9 +382,11 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
                 }
                 ++sp;
                 cur = lfirst ? left_child<DIM>(nd) : right_child<DIM>(nd);
+                if (cur.ref >= 0) nd_side = lfirst ? 0 : 1;
                 descend = true;
             } else if (nl || nr) {
                 cur = nl ? left_child<DIM>(nd) : right_child<DIM>(nd);
+                if (cur.ref >= 0) nd_side = nl ? 0 : 1;
                 descend = true;
             }
         }
