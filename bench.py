@@ -239,11 +239,17 @@ def alu_ops_per_query(per_q: dict) -> float:
 
 
 def load_traffic():
-    """Per-launch DRAM bytes of the k-NN kernel from the committed ncu capture, if any."""
-    for p in sorted((ROOT / "profiles").glob("*ncu_knn*.json"), reverse=True):
+    """Per-launch DRAM bytes of the main k-NN kernel (the longest captured launch) from
+    the newest committed ncu summary under profiles/, if any."""
+    files = sorted((ROOT / "profiles").glob("*ncu_knn*.json"), key=lambda p: p.stat().st_mtime, reverse=True)
+    for p in files:
         try:
             d = json.loads(p.read_text())
-            return d.get("dram_bytes_per_launch"), p.name
+            ks = [k for k in d.get("kernels", []) if "dram_bytes_per_launch" in k]
+            if not ks:
+                continue
+            main = max(ks, key=lambda k: k.get("gpu__time_duration.sum", [0])[0])
+            return main["dram_bytes_per_launch"], p.name
         except Exception:
             continue
     return None, None
@@ -351,7 +357,8 @@ def run_gpu(args, D: Dist):
         t.zd_free()
         return e0.elapsed_time(e1)
 
-    e2e_step()
+    for _ in range(max(3, args.warmup)):   # warm the host-staging paths (pool growth on first use)
+        e2e_step()
     e2e_ms = []
     D.barrier()
     for _ in range(args.e2e_steps):
