@@ -239,9 +239,15 @@ __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Qu
 // Every lane scans sorted positions [s, e): up to 32 records at a time are staged
 // through shared memory, each lane tests CH of them per uniform pass against its
 // bound, then handles its (few) hits.
+#ifndef ZD_TRANSPOSE_MAX
+#define ZD_TRANSPOSE_MAX 4   // at most this many needing lanes: lanes = candidates
+#endif
 template <int DIM, int K>
-__device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t s, int32_t e, Lane<DIM, K>& L,
-                                          WarpSh<K>& S, int lane) {
+__device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t s, int32_t e, bool need,
+                                          Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
+    const uint32_t M = __ballot_sync(0xffffffffu, need);
+    if (M == 0) return;
+    const int w = __popc(M);
     ZD_STAT(ZS_SPANS, 1);
     for (int32_t b = s; b < e; b += 32) {
         const int n32 = min(32, e - b);
@@ -258,13 +264,35 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                     compact<DIM, K>(L, S, lane);
                 }
             }
-            const int64_t U = L.U;
             uint32_t hit = 0;
+            if (w > ZD_TRANSPOSE_MAX) {
+                // every lane tests every candidate against its own bound
+                const int64_t U = L.U;
 #pragma unroll kUnroll
-            for (int j = 0; j < cnt; ++j) {
-                const int4 c = S.c[h0 + j];
-                const bool h = dist2<DIM>(L.q, c) <= U && c.w != L.q.id;   // self excluded by id
-                hit |= (h ? 1u : 0u) << j;
+                for (int j = 0; j < cnt; ++j) {
+                    const int4 c = S.c[h0 + j];
+                    const bool h = dist2<DIM>(L.q, c) <= U && c.w != L.q.id;   // self excluded by id
+                    hit |= (h ? 1u : 0u) << j;
+                }
+            } else {
+                // few lanes need these candidates: lane j holds candidate j and the warp
+                // loops over the needing queries (broadcast by shuffle), one ballot each
+                const bool cv = lane < cnt;
+                const int4 c = S.c[h0 + (cv ? lane : 0)];
+                uint32_t m = M;
+                while (m) {
+                    const int i = __ffs(m) - 1;
+                    m &= m - 1;
+                    Query<DIM> qi;
+                    qi.c[0] = __shfl_sync(0xffffffffu, L.q.c[0], i);
+                    qi.c[1] = __shfl_sync(0xffffffffu, L.q.c[1], i);
+                    qi.c[2] = DIM == 3 ? __shfl_sync(0xffffffffu, L.q.c[2], i) : 0;
+                    const int32_t idi = __shfl_sync(0xffffffffu, L.q.id, i);
+                    const int64_t Ui = __shfl_sync(0xffffffffu, L.U, i);
+                    const bool h = cv && dist2<DIM>(qi, c) <= Ui && c.w != idi;
+                    const uint32_t B = __ballot_sync(0xffffffffu, h);
+                    if (lane == i) hit = B;
+                }
             }
 #ifdef ZD_KNN_STATS
             {
@@ -282,13 +310,12 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 const int64_t d = dist2<DIM>(L.q, S.c[j]);
                 if (d > L.U) continue;   // the bound shrank since the uniform pass
                 const float xf = __ll2float_ru(d);
-                float x = xf;
+                // sorted insertion of xf, dropping the largest: every new slot is the
+                // median of (fa[t-1], xf, fa[t]) — all slots independent (depth 2)
+                // instead of a K-long compare-exchange chain
 #pragma unroll
-                for (int t = 0; t < K; ++t) {
-                    const float lo = fminf(L.fa[t], x);
-                    x = fmaxf(L.fa[t], x);
-                    L.fa[t] = lo;
-                }
+                for (int t = K - 1; t > 0; --t) L.fa[t] = fmaxf(L.fa[t - 1], fminf(L.fa[t], xf));
+                L.fa[0] = fminf(L.fa[0], xf);
                 set_bound<DIM, K>(L);
                 S.bp[L.cnt][lane] = b + j;
                 S.bf[L.cnt][lane] = xf;
@@ -301,12 +328,14 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
 // scan [s, e) minus the already scanned span [ps_lo, ps_hi) (a union of whole leaves)
 template <int DIM, int K>
 __device__ __forceinline__ void scan_leaves(const int4* __restrict__ recs, int32_t s, int32_t mid, int32_t e,
-                                            int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
-    // [s, mid) and [mid, e) are whole leaves (mid == e for a single leaf)
+                                            bool needl, bool needr, int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L,
+                                            WarpSh<K>& S, int lane) {
+    // [s, mid) and [mid, e) are whole leaves (mid == e for a single leaf); a lane that
+    // needs either leaf tests both
     const bool skip_l = s >= ps_lo && s < ps_hi;
     const bool skip_r = mid < e && mid >= ps_lo && mid < ps_hi;
     const int32_t a = skip_l ? mid : s, b = skip_r ? mid : e;
-    if (a < b) scan_span<DIM, K>(recs, a, b, L, S, lane);
+    if (a < b) scan_span<DIM, K>(recs, a, b, (!skip_l && needl) || (!skip_r && needr), L, S, lane);
 }
 
 #ifndef ZD_LOOKAHEAD
@@ -329,14 +358,15 @@ __device__ __forceinline__ void unpack_box(const StkEntry& e, int32_t (&bx)[2 * 
 // Joint Alg. 2 over the subtree `cur`; the span [ps_lo, ps_hi) was scanned already.
 template <int DIM, int K>
 __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const Node<DIM>* __restrict__ nodes, Ref cur,
-                                           int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
+                                           bool cur_need, int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L,
+                                           WarpSh<K>& S, int lane) {
     constexpr int NW = (int)(sizeof(Node<DIM>) / 16);
     int sp = 0;
     int nd_side = -1;   // >= 0: cur's node is (arriving) in S.nbuf[nd_side]
     while (true) {
         bool descend = false;
         if (cur.ref < 0) {
-            scan_leaves<DIM, K>(recs, ~cur.ref, cur.end, cur.end, ps_lo, ps_hi, L, S, lane);
+            scan_leaves<DIM, K>(recs, ~cur.ref, cur.end, cur.end, cur_need, false, ps_lo, ps_hi, L, S, lane);
         } else {
             ZD_STAT(ZS_NODES, 1);
             Node<DIM> nd;
@@ -362,10 +392,11 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
             }
             const int64_t w = L.U;
             const int64_t dl = boxd2<DIM>(L.q, nd.lbox), dr = boxd2<DIM>(L.q, nd.rbox);
-            const bool nl = __any_sync(0xffffffffu, dl <= w), nr = __any_sync(0xffffffffu, dr <= w);
+            const bool ln = dl <= w, rn = dr <= w;
+            const bool nl = __any_sync(0xffffffffu, ln), nr = __any_sync(0xffffffffu, rn);
             if (nl && nr && nd.left < 0 && nd.right < 0) {
                 // two leaf children: one contiguous span [start, end) of <= 2 leaves
-                scan_leaves<DIM, K>(recs, ~nd.left, nd.mid, ~nd.right, ps_lo, ps_hi, L, S, lane);
+                scan_leaves<DIM, K>(recs, ~nd.left, nd.mid, ~nd.right, ln, rn, ps_lo, ps_hi, L, S, lane);
             } else if (nl && nr) {
                 // visit first the child nearer for most lanes (performance only, reading 10)
                 const bool lfirst = __popc(__ballot_sync(0xffffffffu, dl <= dr)) >= 16;
@@ -382,10 +413,12 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
                 }
                 ++sp;
                 cur = lfirst ? left_child<DIM>(nd) : right_child<DIM>(nd);
+                cur_need = lfirst ? ln : rn;
                 if (cur.ref >= 0) nd_side = lfirst ? 0 : 1;
                 descend = true;
             } else if (nl || nr) {
                 cur = nl ? left_child<DIM>(nd) : right_child<DIM>(nd);
+                cur_need = nl ? ln : rn;
                 if (cur.ref >= 0) nd_side = nl ? 0 : 1;
                 descend = true;
             }
@@ -400,8 +433,10 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
             const StkEntry e = S.stk[sp];
             int32_t bx[2 * DIM];
             unpack_box<DIM>(e, bx);
-            if (__any_sync(0xffffffffu, boxd2<DIM>(L.q, bx) <= L.U)) {
+            const bool pn = boxd2<DIM>(L.q, bx) <= L.U;
+            if (__any_sync(0xffffffffu, pn)) {
                 cur = Ref{e.a.x, e.b.w};
+                cur_need = pn;
                 found = true;
                 break;
             }
@@ -479,7 +514,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         if (lB - lA > 8) lB = lA;
     }
     const int32_t ps_lo = __ldg(A.leaf_start + lA), ps_hi = __ldg(A.leaf_start + lB + 1);
-    scan_span<DIM, K>(A.recs, ps_lo, ps_hi, L, S, lane);
+    scan_span<DIM, K>(A.recs, ps_lo, ps_hi, active, L, S, lane);
 
     if (can_defer) {
         // A packet whose queries are far apart compared with their neighbour distances
@@ -529,6 +564,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
     // C = the node whose subtree has been searched (-1: the single leaf lA)
     int32_t C = -1, P;
     Ref sub{kNoSub, 0};
+    bool sub_need = active;
     if (lA == lB) {
         P = __ldg(A.leaf_parent + lA);
     } else {
@@ -551,7 +587,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         sub = Ref{x, 0};
     }
     while (true) {
-        if (sub.ref != kNoSub) joint_down<DIM, K>(A.recs, nodes, sub, ps_lo, ps_hi, L, S, lane);
+        if (sub.ref != kNoSub) joint_down<DIM, K>(A.recs, nodes, sub, sub_need, ps_lo, ps_hi, L, S, lane);
         if (P < 0) break;
         ZD_STAT(ZS_ASCENTS, 1);
         const Node<DIM> nd = load_node<DIM>(nodes + P);
@@ -564,7 +600,8 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         }
         const int64_t w = L.U;
         if (__all_sync(0xffffffffu, stop_at<DIM>(L.q, cb, w))) break;
-        sub = __any_sync(0xffffffffu, boxd2<DIM>(L.q, sb) <= w) ? (isl ? right_child<DIM>(nd) : left_child<DIM>(nd))
+        sub_need = boxd2<DIM>(L.q, sb) <= w;
+        sub = __any_sync(0xffffffffu, sub_need) ? (isl ? right_child<DIM>(nd) : left_child<DIM>(nd))
                                                               : Ref{kNoSub, 0};
         C = P;
         P = nd.parent;
