@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <mutex>
 #include <vector>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <utility>
@@ -448,6 +449,12 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
     a.hard_count = hard;
     a.hard_list = hard + 2;
     a.hard_cap = kHardCap;
+    // ZD_KNN_DEFER (testing): "none" = no second pass, "all" = every packet deferred
+    // (up to the list capacity); default: incoherent packets only
+    if (const char* dm = std::getenv("ZD_KNN_DEFER")) {
+        if (!std::strcmp(dm, "none")) a.hard_list = nullptr;
+        else if (!std::strcmp(dm, "all")) a.defer_all = 1;
+    }
     a.dim = h->dim; a.k = k; a.n = h->n;
     a.recs = h->recs; a.pt_leaf = h->tb.pt_leaf; a.leaf_start = h->tb.leaf_start;
     a.leaf_parent = h->tb.leaf_parent; a.nodes = h->tb.nodes; a.node_range = h->tb.range;

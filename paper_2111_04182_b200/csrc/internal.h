@@ -67,6 +67,7 @@ struct KnnArgs {
     int32_t* hard_list;          // [hard_cap] scratch for deferred packets (NULL: none)
     int32_t* hard_count;         // zeroed by the caller
     int hard_cap;
+    int defer_all;               // testing: every packet goes to the second pass
 };
 int knn_kmax();
 // Work counters of the packet k-NN kernel (only in a -DZD_KNN_STATS build).

@@ -463,6 +463,7 @@ struct PacketArgs {
     int32_t* hard_count;
     int hard_cap;
     int hard_mode;             // 0: packets; 1: second pass over the deferred packets' queries
+    int defer_all;             // testing: defer every packet (hard_list must be set)
 };
 
 #ifndef ZD_INCOHERENT
@@ -549,7 +550,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
             }
         }
         const float med = __shfl_sync(0xffffffffu, v, nact >> 1);
-        if (nfin == nact && ext2 > ZD_INCOHERENT * exp2f(med)) {
+        if (A.defer_all || (nfin == nact && ext2 > ZD_INCOHERENT * exp2f(med))) {
             int slot = 0;
             if (lane == 0) slot = atomicAdd(A.hard_count, 1);
             slot = __shfl_sync(0xffffffffu, slot, 0);
@@ -694,6 +695,7 @@ PacketArgs packet_args(const KnnArgs& a) {
     A.nodes = a.nodes; A.node_range = a.node_range; A.split_bit = a.split_bit;
     A.k = a.k; A.row_of_id = a.row_of_id; A.out_idx = a.out_idx; A.out_d2 = a.out_d2;
     A.hard_list = a.hard_list; A.hard_count = a.hard_count; A.hard_cap = a.hard_cap; A.hard_mode = 0;
+    A.defer_all = a.defer_all;
     return A;
 }
 

@@ -277,3 +277,22 @@ def test_streams_and_timing(zd, oracle_mod):
     assert tm["knn"] > 0
     ri, rd, _ = oracle_mod.Tree(pts).knn_all(10)
     check_rows(oi.cpu().numpy(), od.cpu().numpy(), ri, rd)
+
+
+@pytest.mark.parametrize("mode", ["none", "all"])
+@pytest.mark.parametrize("dist,dim", [("uniform", 2), ("uniform", 3), ("plummer", 3), ("sphere", 3), ("dup", 3)])
+def test_knn_deferral_modes(zd, oracle_mod, monkeypatch, mode, dist, dim):
+    """The k-NN kernel's second pass (packets deferred as incoherent, searched one query
+    per warp) and the single-pass path both give the oracle's rows: ZD_KNN_DEFER=all
+    sends every packet through the second pass, =none disables it."""
+    monkeypatch.setenv("ZD_KNN_DEFER", mode)
+    pts = zdgen.points(dist, 12000, dim, seed=21)
+    t = zd.zd_build(dev(pts))
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(10)
+    check_rows(gi, gd, oi, od)
+    q = zdgen.uniform(3000, dim, seed=22)
+    qi, qd = t.zd_knn(10, queries=dev(q))
+    torch.cuda.synchronize()
+    oqi, oqd, _ = oracle_mod.Tree(pts).knn_queries(q, 10)
+    check_rows(qi.cpu().numpy(), qd.cpu().numpy(), oqi, oqd)
