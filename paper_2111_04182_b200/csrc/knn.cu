@@ -143,7 +143,7 @@ struct Pw {
     static constexpr int v = K <= 16 ? ZD_PW : 2;   // warps per block (shared memory grows with K)
 };
 #ifndef ZD_MINB
-#define ZD_MINB 6         // min resident blocks per SM for K <= 10 (register budget)
+#define ZD_MINB 7         // min resident blocks per SM for K <= 10 (register budget)
 #endif
 constexpr int CH = 16;                   // candidates tested per uniform pass
 constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
@@ -153,11 +153,11 @@ constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
 constexpr int kStk = ZD_STK;             // per-warp stack entries (>= tree height; 64 = key bits + 1)
 
 #ifndef ZD_CAP_MIN
-#define ZD_CAP_MIN 26
+#define ZD_CAP_MIN 22
 #endif
 template <int K>
-struct Cap {
-    static constexpr int v = (K + CH > ZD_CAP_MIN) ? K + CH : ZD_CAP_MIN;   // buffered candidates per lane
+struct Cap {   // buffered candidates per lane (overflow compacts per lane: any value > K works)
+    static constexpr int v = (K + 8 > ZD_CAP_MIN) ? K + 8 : ZD_CAP_MIN;
 };
 
 // A child reference in traversal form: ref >= 0 internal node; ref < 0 a leaf with
@@ -177,13 +177,25 @@ struct alignas(16) StkEntry {
     int4 a, b;          // a = (ref, box words 0..2), b = (box words 3..5, leaf end)
 };
 
+#ifndef ZD_STK16
+#define ZD_STK16 1   // 16-byte stack entries; the far child's box is re-read from its parent
+#endif
+#ifndef ZD_F32FILTER
+#define ZD_F32FILTER 1   // 3D: candidate tests in fp32 (exact coordinates), confirmed in int64
+#endif
 template <int K>
 struct WarpSh {
     int4 c[32];                          // staged candidates (x, y, z|0, id)
+#if ZD_F32FILTER
+    float4 f[32];                        // 3D: the same in fp32 (exact below 2^24)
+#endif
     int32_t bp[Cap<K>::v][32];           // per-lane buffered positions; column = lane
     float bf[Cap<K>::v][32];             //   ... and their d2 rounded up to fp32
+#if ZD_STK16
+    int4 stk[kStk];                      // (ref, leaf end, parent node, side): box reloaded on pop
+#else
     StkEntry stk[kStk];
-    int4 nbuf[2][4];                     // lookahead: the current node's children (cp.async)
+#endif
 };
 
 template <int DIM, int K>
@@ -191,6 +203,8 @@ struct Lane {
     Query<DIM> q;
     float fa[K];
     int64_t U;          // -1 for an idle lane: needs nothing, accepts nothing
+    float qf[3];        // 3D fp32 filter: the query in fp32 (exact)
+    float wb;           //   and a bound with d2 <= U  =>  fp32 d2 <= wb
     int cnt;
 };
 
@@ -198,6 +212,10 @@ template <int DIM, int K>
 __device__ __forceinline__ void set_bound(Lane<DIM, K>& L) {
     const float f = L.fa[K - 1];
     L.U = (f == INFINITY) ? INT64_MAX : __float2ll_ru(f);
+    // 3D: coordinates and their differences are exact in fp32 and the three rounded
+    // products/sums make the fp32 d2 at most (1 + 3.0000002 * 2^-24) times the exact
+    // one, so d2 <= U = f implies fp32 d2 <= f * (1 + 2^-21) rounded up
+    if (DIM == 3) L.wb = __fmul_ru(f, 1.0f + 0x1p-21f);
 }
 
 // Drop buffered candidates that can no longer qualify: a final neighbour p has
@@ -239,6 +257,9 @@ __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Qu
 // Every lane scans sorted positions [s, e): up to 32 records at a time are staged
 // through shared memory, each lane tests CH of them per uniform pass against its
 // bound, then handles its (few) hits.
+#ifndef ZD_SLACK
+#define ZD_SLACK 4          // uniform compaction when a needing lane has > CAP - SLACK entries
+#endif
 #ifndef ZD_TRANSPOSE_MAX
 #define ZD_TRANSPOSE_MAX 4   // at most this many needing lanes: lanes = candidates
 #endif
@@ -252,34 +273,74 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
     for (int32_t b = s; b < e; b += 32) {
         const int n32 = min(32, e - b);
         __syncwarp();
-        if (lane < n32) S.c[lane] = __ldg(recs + b + lane);
+        if (lane < n32) {
+            const int4 r = __ldg(recs + b + lane);
+            S.c[lane] = r;
+#if ZD_F32FILTER
+            if (DIM == 3)
+                S.f[lane] = make_float4(__int2float_rn(r.x), __int2float_rn(r.y), __int2float_rn(r.z), __int_as_float(r.w));
+#endif
+        }
         __syncwarp();
         for (int h0 = 0; h0 < n32; h0 += CH) {
             const int cnt = min(CH, n32 - h0);
-            if (__any_sync(0xffffffffu, L.cnt + cnt > Cap<K>::v)) {
+            // compact (all lanes together) once some needing lane is nearly full; a lane
+            // that still fills up while taking hits compacts on its own (take_hit)
+            if (__any_sync(0xffffffffu, need && L.cnt > Cap<K>::v - ZD_SLACK)) {
                 ZD_STAT(ZS_COMPACT, 1);
                 compact<DIM, K>(L, S, lane);
-                if (L.cnt + cnt > Cap<K>::v) {
-                    mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
-                    compact<DIM, K>(L, S, lane);
-                }
             }
             uint32_t hit = 0;
             if (w > ZD_TRANSPOSE_MAX) {
                 // every lane tests every candidate against its own bound
-                const int64_t U = L.U;
+#if ZD_F32FILTER
+                if (DIM == 3) {
+                    const float wb = L.wb;
 #pragma unroll kUnroll
-                for (int j = 0; j < cnt; ++j) {
-                    const int4 c = S.c[h0 + j];
-                    const bool h = dist2<DIM>(L.q, c) <= U && c.w != L.q.id;   // self excluded by id
-                    hit |= (h ? 1u : 0u) << j;
+                    for (int j = 0; j < cnt; ++j) {
+                        const float4 c = S.f[h0 + j];
+                        const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
+                        const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                        const bool h = df <= wb && __float_as_int(c.w) != L.q.id;   // self excluded by id
+                        hit |= (h ? 1u : 0u) << j;
+                    }
+                } else
+#endif
+                {
+                    const int64_t U = L.U;
+#pragma unroll kUnroll
+                    for (int j = 0; j < cnt; ++j) {
+                        const int4 c = S.c[h0 + j];
+                        const bool h = dist2<DIM>(L.q, c) <= U && c.w != L.q.id;   // self excluded by id
+                        hit |= (h ? 1u : 0u) << j;
+                    }
                 }
             } else {
                 // few lanes need these candidates: lane j holds candidate j and the warp
                 // loops over the needing queries (broadcast by shuffle), one ballot each
                 const bool cv = lane < cnt;
-                const int4 c = S.c[h0 + (cv ? lane : 0)];
                 uint32_t m = M;
+#if ZD_F32FILTER
+                if (DIM == 3) {
+                    const float4 c = S.f[h0 + (cv ? lane : 0)];
+                    while (m) {
+                        const int i = __ffs(m) - 1;
+                        m &= m - 1;
+                        const float qx = __shfl_sync(0xffffffffu, L.qf[0], i);
+                        const float qy = __shfl_sync(0xffffffffu, L.qf[1], i);
+                        const float qz = __shfl_sync(0xffffffffu, L.qf[2], i);
+                        const float wbi = __shfl_sync(0xffffffffu, L.wb, i);
+                        const int32_t idi = __shfl_sync(0xffffffffu, L.q.id, i);
+                        const float dx = qx - c.x, dy = qy - c.y, dz = qz - c.z;
+                        const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                        const bool h = cv && df <= wbi && __float_as_int(c.w) != idi;
+                        const uint32_t B = __ballot_sync(0xffffffffu, h);
+                        if (lane == i) hit = B;
+                    }
+                    m = 0;
+                }
+#endif
+                const int4 c = S.c[h0 + (cv ? lane : 0)];
                 while (m) {
                     const int i = __ffs(m) - 1;
                     m &= m - 1;
@@ -317,6 +378,13 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 for (int t = K - 1; t > 0; --t) L.fa[t] = fmaxf(L.fa[t - 1], fminf(L.fa[t], xf));
                 L.fa[0] = fminf(L.fa[0], xf);
                 set_bound<DIM, K>(L);
+                if (L.cnt == Cap<K>::v) {   // rare: per-lane compaction
+                    compact<DIM, K>(L, S, lane);
+                    if (L.cnt == Cap<K>::v) {   // massive ties: keep only the exact K best
+                        mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
+                        compact<DIM, K>(L, S, lane);
+                    }
+                }
                 S.bp[L.cnt][lane] = b + j;
                 S.bf[L.cnt][lane] = xf;
                 ++L.cnt;
@@ -338,16 +406,6 @@ __device__ __forceinline__ void scan_leaves(const int4* __restrict__ recs, int32
     if (a < b) scan_span<DIM, K>(recs, a, b, (!skip_l && needl) || (!skip_r && needr), L, S, lane);
 }
 
-#ifndef ZD_LOOKAHEAD
-#define ZD_LOOKAHEAD 0
-#endif
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
 template <int DIM>
 __device__ __forceinline__ void unpack_box(const StkEntry& e, int32_t (&bx)[2 * DIM]) {
     const int w[6] = {e.a.y, e.a.z, e.a.w, e.b.x, e.b.y, e.b.z};
@@ -360,36 +418,14 @@ template <int DIM, int K>
 __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const Node<DIM>* __restrict__ nodes, Ref cur,
                                            bool cur_need, int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L,
                                            WarpSh<K>& S, int lane) {
-    constexpr int NW = (int)(sizeof(Node<DIM>) / 16);
     int sp = 0;
-    int nd_side = -1;   // >= 0: cur's node is (arriving) in S.nbuf[nd_side]
     while (true) {
         bool descend = false;
         if (cur.ref < 0) {
             scan_leaves<DIM, K>(recs, ~cur.ref, cur.end, cur.end, cur_need, false, ps_lo, ps_hi, L, S, lane);
         } else {
             ZD_STAT(ZS_NODES, 1);
-            Node<DIM> nd;
-            if (ZD_LOOKAHEAD && nd_side >= 0) {
-                cp_async_wait();
-                __syncwarp();
-                int4* d = reinterpret_cast<int4*>(&nd);
-#pragma unroll
-                for (int t = 0; t < NW; ++t) d[t] = S.nbuf[nd_side][t];
-            } else {
-                nd = load_node<DIM>(nodes + cur.ref);
-            }
-            nd_side = -1;
-            if (ZD_LOOKAHEAD) {
-                // copy the internal children's nodes to shared memory while testing boxes
-                cp_async_wait();
-                __syncwarp();
-                if (nd.left >= 0 && lane < NW)
-                    cp_async16(&S.nbuf[0][lane], reinterpret_cast<const int4*>(nodes + nd.left) + lane);
-                if (nd.right >= 0 && lane >= 4 && lane < 4 + NW)
-                    cp_async16(&S.nbuf[1][lane - 4], reinterpret_cast<const int4*>(nodes + nd.right) + (lane - 4));
-                cp_async_commit();
-            }
+            const Node<DIM> nd = load_node<DIM>(nodes + cur.ref);
             const int64_t w = L.U;
             const int64_t dl = boxd2<DIM>(L.q, nd.lbox), dr = boxd2<DIM>(L.q, nd.rbox);
             const bool ln = dl <= w, rn = dr <= w;
@@ -403,6 +439,9 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
                 const Ref far = lfirst ? right_child<DIM>(nd) : left_child<DIM>(nd);
                 __syncwarp();
                 if (lane == 0) {
+#if ZD_STK16
+                    S.stk[sp] = make_int4(far.ref, far.end, cur.ref, lfirst ? 1 : 0);
+#else
                     int w6[6] = {0, 0, 0, 0, 0, 0};
 #pragma unroll
                     for (int a = 0; a < 2 * DIM; ++a) w6[a] = lfirst ? nd.rbox[a] : nd.lbox[a];
@@ -410,16 +449,15 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
                     e.a = make_int4(far.ref, w6[0], w6[1], w6[2]);
                     e.b = make_int4(w6[3], w6[4], w6[5], far.end);
                     S.stk[sp] = e;
+#endif
                 }
                 ++sp;
                 cur = lfirst ? left_child<DIM>(nd) : right_child<DIM>(nd);
                 cur_need = lfirst ? ln : rn;
-                if (cur.ref >= 0) nd_side = lfirst ? 0 : 1;
                 descend = true;
             } else if (nl || nr) {
                 cur = nl ? left_child<DIM>(nd) : right_child<DIM>(nd);
                 cur_need = nl ? ln : rn;
-                if (cur.ref >= 0) nd_side = nl ? 0 : 1;
                 descend = true;
             }
         }
@@ -430,12 +468,28 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
         while (sp > 0) {
             --sp;
             ZD_STAT(ZS_POPS, 1);
-            const StkEntry e = S.stk[sp];
             int32_t bx[2 * DIM];
+#if ZD_STK16
+            const int4 e = S.stk[sp];
+            {
+                // the far child's box: right box (side 1) or left box of its parent node
+                const int2* pb = reinterpret_cast<const int2*>(nodes + e.z) + (e.w ? DIM : 0);
+#pragma unroll
+                for (int t = 0; t < DIM; ++t) {
+                    const int2 v = __ldg(pb + t);
+                    bx[2 * t] = v.x;
+                    bx[2 * t + 1] = v.y;
+                }
+            }
+            const Ref popped{e.x, e.y};
+#else
+            const StkEntry e = S.stk[sp];
             unpack_box<DIM>(e, bx);
+            const Ref popped{e.a.x, e.b.w};
+#endif
             const bool pn = boxd2<DIM>(L.q, bx) <= L.U;
             if (__any_sync(0xffffffffu, pn)) {
-                cur = Ref{e.a.x, e.b.w};
+                cur = popped;
                 cur_need = pn;
                 found = true;
                 break;
@@ -494,6 +548,8 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
 #pragma unroll
     for (int t = 0; t < K; ++t) L.fa[t] = INFINITY;
     L.U = active ? INT64_MAX : (int64_t)-1;   // an idle lane needs nothing, accepts nothing
+    L.qf[0] = __int2float_rn(r.x); L.qf[1] = __int2float_rn(r.y); L.qf[2] = __int2float_rn(r.z);
+    L.wb = active ? INFINITY : -1.0f;
     L.cnt = 0;
 
     int32_t lA, lB;

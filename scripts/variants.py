@@ -31,7 +31,7 @@ def run(configs):
     for name in VARIANTS:
         so = ROOT / "build_var" / f"{name}.so"
         env = dict(os.environ, ZD_LIB=str(so))
-        r = subprocess.run([sys.executable, str(ROOT / "scripts" / "probe.py"), "--configs", configs, "--reps", "2"],
+        r = subprocess.run([sys.executable, str(ROOT / "scripts" / "probe.py"), "--configs", configs, "--reps", "3"],
                            env=env, capture_output=True, text=True)
         for line in r.stdout.splitlines():
             if line.startswith("{"):
