@@ -91,9 +91,13 @@ template <int DIM> __device__ __forceinline__ bool in_universe(int x, int y, int
 // mid = first sorted position of the right subtree (= leaf_start[i+1]).  The split
 // bit lives in a separate array (TreeBufs::split_bit); zd_export converts to the
 // documented leaf-index form.
+// Box coordinates: int32 in 2D (30-bit grid); fp32 in 3D, where every 21-bit grid
+// coordinate is exact and the query's fp32 box tests have a proven error bound.
+template <int DIM> struct BoxT { using T = int32_t; };
+template <> struct BoxT<3> { using T = float; };
 template <int DIM> struct alignas(16) Node {
-    int32_t lbox[2 * DIM];   // lo[DIM], hi[DIM]
-    int32_t rbox[2 * DIM];
+    typename BoxT<DIM>::T lbox[2 * DIM];   // lo[DIM], hi[DIM]
+    typename BoxT<DIM>::T rbox[2 * DIM];
     int32_t left, right, parent, mid;
 };
 static_assert(sizeof(Node<2>) == 48, "Node<2> layout");

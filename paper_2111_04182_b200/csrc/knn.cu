@@ -211,18 +211,75 @@ struct Lane {
 template <int DIM, int K>
 __device__ __forceinline__ void set_bound(Lane<DIM, K>& L) {
     const float f = L.fa[K - 1];
-    L.U = (f == INFINITY) ? INT64_MAX : __float2ll_ru(f);
-    // 3D: coordinates and their differences are exact in fp32 and the three rounded
-    // products/sums make the fp32 d2 at most (1 + 3.0000002 * 2^-24) times the exact
-    // one, so d2 <= U = f implies fp32 d2 <= f * (1 + 2^-21) rounded up
-    if (DIM == 3) L.wb = __fmul_ru(f, 1.0f + 0x1p-21f);
+    if (DIM == 3) {
+        // 3D: coordinates and their differences are exact in fp32 and the three rounded
+        // products/sums make the fp32 d2 at most (1 + 3.0000002 * 2^-24) times the
+        // exact one, so d2 <= f implies fp32 d2 <= f * (1 + 2^-21) rounded up
+        L.wb = __fmul_ru(f, 1.0f + 0x1p-21f);
+    } else {
+        L.U = (f == INFINITY) ? INT64_MAX : __float2ll_ru(f);
+    }
+}
+
+// Is the lane's bound reached by the box (reading 8: visit iff box d2 <= bound)?
+// 3D in fp32: per axis max(lo - q, 0) + max(q - hi, 0) is exact, the sum of squares
+// errs like a candidate distance, so the test against wb is conservative.
+template <int DIM, int K>
+__device__ __forceinline__ bool box_need(const Lane<DIM, K>& L, const typename BoxT<DIM>::T* b) {
+    if constexpr (DIM == 3) {
+        float df = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float t = fmaxf(b[a] - L.qf[a], 0.f) + fmaxf(L.qf[a] - b[3 + a], 0.f);
+            df = fmaf(t, t, df);
+        }
+        return df <= L.wb;
+    } else {
+        return boxd2<DIM>(L.q, b) <= L.U;
+    }
+}
+
+// fp32 (3D) or exact (2D) box distance, for the nearer-child order only
+template <int DIM, int K>
+__device__ __forceinline__ float box_order(const Lane<DIM, K>& L, const typename BoxT<DIM>::T* b) {
+    if constexpr (DIM == 3) {
+        float df = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float t = fmaxf(b[a] - L.qf[a], 0.f) + fmaxf(L.qf[a] - b[3 + a], 0.f);
+            df = fmaf(t, t, df);
+        }
+        return df;
+    } else {
+        return (float)boxd2<DIM>(L.q, b);
+    }
+}
+
+// Alg. 3 stop test (reading 9) on C's box: q inside with margin m on every axis and
+// (m+1)^2 > the lane's bound; an idle lane always stops.  3D: m is exact in fp32 and
+// (m+1)^2 is rounded down, so the test never stops too early.
+template <int DIM, int K>
+__device__ __forceinline__ bool lane_stop(const Lane<DIM, K>& L, const typename BoxT<DIM>::T* b) {
+    if constexpr (DIM == 3) {
+        if (L.wb < 0.f) return true;
+        float m = INFINITY;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) m = fminf(m, fminf(L.qf[a] - b[a], b[3 + a] - L.qf[a]));
+        if (m < 0.f) return false;
+        const float mm = m + 1.0f;
+        return __fmul_rd(mm, mm) > L.fa[K - 1];
+    } else {
+        return stop_at<DIM>(L.q, b, L.U);
+    }
 }
 
 // Drop buffered candidates that can no longer qualify: a final neighbour p has
 // d2(p) <= the exact k-th smallest d2 seen so far, hence ru(d2(p)) <= fa[K-1].
 template <int DIM, int K>
 __device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
-    const float F = L.fa[K - 1];
+    // 3D buffers fp32-derived upper bounds ub with d2 <= ub <= d2 (1 + 2^-20): a final
+    // neighbour has ub <= D_k (1 + 2^-20) <= fa[K-1] (1 + 2^-20)
+    const float F = DIM == 3 ? __fmul_ru(L.fa[K - 1], 1.0f + 0x1p-20f) : L.fa[K - 1];
     int w = 0;
     for (int e = 0; e < L.cnt; ++e) {
         const float f = S.bf[e][lane];
@@ -368,9 +425,21 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
             while (hit) {
                 const int j = h0 + __ffs(hit) - 1;
                 hit &= hit - 1;
-                const int64_t d = dist2<DIM>(L.q, S.c[j]);
-                if (d > L.U) continue;   // the bound shrank since the uniform pass
-                const float xf = __ll2float_ru(d);
+                float xf;
+#if ZD_F32FILTER
+                if (DIM == 3) {
+                    const float4 c = S.f[j];
+                    const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
+                    const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                    if (df > L.wb) continue;   // the bound shrank since the test
+                    xf = __fmul_ru(df, 1.0f + 0x1p-21f);   // >= the exact d2
+                } else
+#endif
+                {
+                    const int64_t d = dist2<DIM>(L.q, S.c[j]);
+                    if (d > L.U) continue;   // the bound shrank since the test
+                    xf = __ll2float_ru(d);
+                }
                 // sorted insertion of xf, dropping the largest: every new slot is the
                 // median of (fa[t-1], xf, fa[t]) — all slots independent (depth 2)
                 // instead of a K-long compare-exchange chain
@@ -426,16 +495,15 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
         } else {
             ZD_STAT(ZS_NODES, 1);
             const Node<DIM> nd = load_node<DIM>(nodes + cur.ref);
-            const int64_t w = L.U;
-            const int64_t dl = boxd2<DIM>(L.q, nd.lbox), dr = boxd2<DIM>(L.q, nd.rbox);
-            const bool ln = dl <= w, rn = dr <= w;
+            const bool ln = box_need<DIM, K>(L, nd.lbox), rn = box_need<DIM, K>(L, nd.rbox);
             const bool nl = __any_sync(0xffffffffu, ln), nr = __any_sync(0xffffffffu, rn);
             if (nl && nr && nd.left < 0 && nd.right < 0) {
                 // two leaf children: one contiguous span [start, end) of <= 2 leaves
                 scan_leaves<DIM, K>(recs, ~nd.left, nd.mid, ~nd.right, ln, rn, ps_lo, ps_hi, L, S, lane);
             } else if (nl && nr) {
                 // visit first the child nearer for most lanes (performance only, reading 10)
-                const bool lfirst = __popc(__ballot_sync(0xffffffffu, dl <= dr)) >= 16;
+                const bool lfirst =
+                    __popc(__ballot_sync(0xffffffffu, box_order<DIM, K>(L, nd.lbox) <= box_order<DIM, K>(L, nd.rbox))) >= 16;
                 const Ref far = lfirst ? right_child<DIM>(nd) : left_child<DIM>(nd);
                 __syncwarp();
                 if (lane == 0) {
@@ -468,26 +536,27 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
         while (sp > 0) {
             --sp;
             ZD_STAT(ZS_POPS, 1);
-            int32_t bx[2 * DIM];
+            typename BoxT<DIM>::T bx[2 * DIM];
 #if ZD_STK16
             const int4 e = S.stk[sp];
             {
                 // the far child's box: right box (side 1) or left box of its parent node
-                const int2* pb = reinterpret_cast<const int2*>(nodes + e.z) + (e.w ? DIM : 0);
+                const Node<DIM>* pn_node = nodes + e.z;
 #pragma unroll
-                for (int t = 0; t < DIM; ++t) {
-                    const int2 v = __ldg(pb + t);
-                    bx[2 * t] = v.x;
-                    bx[2 * t + 1] = v.y;
-                }
+                for (int t = 0; t < 2 * DIM; ++t) bx[t] = __ldg(e.w ? &pn_node->rbox[t] : &pn_node->lbox[t]);
             }
             const Ref popped{e.x, e.y};
 #else
             const StkEntry e = S.stk[sp];
-            unpack_box<DIM>(e, bx);
+            {
+                int32_t bi[2 * DIM];
+                unpack_box<DIM>(e, bi);
+#pragma unroll
+                for (int t = 0; t < 2 * DIM; ++t) bx[t] = (typename BoxT<DIM>::T)bi[t];
+            }
             const Ref popped{e.a.x, e.b.w};
 #endif
-            const bool pn = boxd2<DIM>(L.q, bx) <= L.U;
+            const bool pn = box_need<DIM, K>(L, bx);
             if (__any_sync(0xffffffffu, pn)) {
                 cur = popped;
                 cur_need = pn;
@@ -590,12 +659,12 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
             const float e = (float)(mx - mn);
             ext2 = fmaxf(ext2, e * e);
         }
-        const bool fin = active && L.U != INT64_MAX;
+        const bool fin = active && L.fa[K - 1] != INFINITY;
         const int nfin = __popc(__ballot_sync(0xffffffffu, fin));
         const int nact = __popc(__ballot_sync(0xffffffffu, active));
         // median over the active lanes of log2(bound + 1) (bitonic sort across the warp;
         // idle lanes sort last)
-        float v = active ? (fin ? __log2f((float)L.U + 1.0f) : 1e30f) : INFINITY;
+        float v = active ? (fin ? __log2f(L.fa[K - 1] + 1.0f) : 1e30f) : INFINITY;
 #pragma unroll
         for (int kk = 2; kk <= 32; kk <<= 1) {
 #pragma unroll
@@ -649,15 +718,14 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         ZD_STAT(ZS_ASCENTS, 1);
         const Node<DIM> nd = load_node<DIM>(nodes + P);
         const bool isl = C >= 0 ? nd.left == C : P == lA;   // leaf l is the left child of node l
-        int32_t cb[2 * DIM], sb[2 * DIM];
+        typename BoxT<DIM>::T cb[2 * DIM], sb[2 * DIM];
 #pragma unroll
         for (int a = 0; a < 2 * DIM; ++a) {
             cb[a] = isl ? nd.lbox[a] : nd.rbox[a];
             sb[a] = isl ? nd.rbox[a] : nd.lbox[a];
         }
-        const int64_t w = L.U;
-        if (__all_sync(0xffffffffu, stop_at<DIM>(L.q, cb, w))) break;
-        sub_need = boxd2<DIM>(L.q, sb) <= w;
+        if (__all_sync(0xffffffffu, lane_stop<DIM, K>(L, cb))) break;
+        sub_need = box_need<DIM, K>(L, sb);
         sub = __any_sync(0xffffffffu, sub_need) ? (isl ? right_child<DIM>(nd) : left_child<DIM>(nd))
                                                               : Ref{kNoSub, 0};
         C = P;

@@ -119,9 +119,9 @@ __global__ void __launch_bounds__(TT) compact_kernel(const uint8_t* __restrict__
 }
 
 template <int DIM>
-__device__ __forceinline__ void store_box(int32_t* dst, const int32_t (&b)[2 * DIM]) {
+__device__ __forceinline__ void store_box(typename BoxT<DIM>::T* dst, const int32_t (&b)[2 * DIM]) {
 #pragma unroll
-    for (int a = 0; a < 2 * DIM; ++a) dst[a] = b[a];
+    for (int a = 0; a < 2 * DIM; ++a) dst[a] = (typename BoxT<DIM>::T)b[a];   // exact (3D: < 2^21)
 }
 
 template <int DIM>
@@ -163,11 +163,11 @@ __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__
             const uint32_t arrived =
                 cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(visit[par]).fetch_add(1u, cuda::memory_order_acq_rel);
             if (arrived == 0) break;   // first child: the sibling finishes the parent
-            const int32_t* sb = as_right ? P->lbox : P->rbox;
+            const typename BoxT<DIM>::T* sb = as_right ? P->lbox : P->rbox;
 #pragma unroll
             for (int a = 0; a < DIM; ++a) {
-                bb[a] = min(bb[a], __ldcg(sb + a));
-                bb[DIM + a] = max(bb[DIM + a], __ldcg(sb + DIM + a));
+                bb[a] = min(bb[a], (int32_t)__ldcg(sb + a));
+                bb[DIM + a] = max(bb[DIM + a], (int32_t)__ldcg(sb + DIM + a));
             }
             if (as_right) L = __ldcg(range + 2 * par); else R = __ldcg(range + 2 * par + 1);
             ref = par;
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) export_nodes_kernel(const Node<DIM>* __re
     const Node<DIM> nd = nodes[i];
     int32_t* o = out + i * (4 * DIM + 4);
 #pragma unroll
-    for (int a = 0; a < 2 * DIM; ++a) { o[a] = nd.lbox[a]; o[2 * DIM + a] = nd.rbox[a]; }
+    for (int a = 0; a < 2 * DIM; ++a) { o[a] = (int32_t)nd.lbox[a]; o[2 * DIM + a] = (int32_t)nd.rbox[a]; }
     o[4 * DIM] = nd.left >= 0 ? nd.left : ~(int32_t)i;             // left leaf child = leaf i
     o[4 * DIM + 1] = nd.right >= 0 ? nd.right : ~(int32_t)(i + 1);  // right leaf child = leaf i+1
     o[4 * DIM + 2] = nd.parent;
