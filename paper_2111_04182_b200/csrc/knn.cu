@@ -221,6 +221,29 @@ __device__ __forceinline__ void set_bound(Lane<DIM, K>& L) {
     }
 }
 
+// Box distance in the lane's test domain: fp32 (3D) or exact int64 (2D).
+template <int DIM> struct BoxD { using T = int64_t; };
+template <> struct BoxD<3> { using T = float; };
+template <int DIM, int K>
+__device__ __forceinline__ typename BoxD<DIM>::T box_dist(const Lane<DIM, K>& L, const typename BoxT<DIM>::T* b) {
+    if constexpr (DIM == 3) {
+        float df = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float t = fmaxf(b[a] - L.qf[a], 0.f) + fmaxf(L.qf[a] - b[3 + a], 0.f);
+            df = fmaf(t, t, df);
+        }
+        return df;
+    } else {
+        return boxd2<DIM>(L.q, b);
+    }
+}
+template <int DIM, int K>
+__device__ __forceinline__ bool within(const Lane<DIM, K>& L, typename BoxD<DIM>::T d) {
+    if constexpr (DIM == 3) return d <= L.wb;
+    else return d <= L.U;
+}
+
 // Is the lane's bound reached by the box (reading 8: visit iff box d2 <= bound)?
 // 3D in fp32: per axis max(lo - q, 0) + max(q - hi, 0) is exact, the sum of squares
 // errs like a candidate distance, so the test against wb is conservative.
@@ -236,22 +259,6 @@ __device__ __forceinline__ bool box_need(const Lane<DIM, K>& L, const typename B
         return df <= L.wb;
     } else {
         return boxd2<DIM>(L.q, b) <= L.U;
-    }
-}
-
-// fp32 (3D) or exact (2D) box distance, for the nearer-child order only
-template <int DIM, int K>
-__device__ __forceinline__ float box_order(const Lane<DIM, K>& L, const typename BoxT<DIM>::T* b) {
-    if constexpr (DIM == 3) {
-        float df = 0.f;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const float t = fmaxf(b[a] - L.qf[a], 0.f) + fmaxf(L.qf[a] - b[3 + a], 0.f);
-            df = fmaf(t, t, df);
-        }
-        return df;
-    } else {
-        return (float)boxd2<DIM>(L.q, b);
     }
 }
 
@@ -495,15 +502,15 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
         } else {
             ZD_STAT(ZS_NODES, 1);
             const Node<DIM> nd = load_node<DIM>(nodes + cur.ref);
-            const bool ln = box_need<DIM, K>(L, nd.lbox), rn = box_need<DIM, K>(L, nd.rbox);
+            const typename BoxD<DIM>::T dl = box_dist<DIM, K>(L, nd.lbox), dr = box_dist<DIM, K>(L, nd.rbox);
+            const bool ln = within<DIM, K>(L, dl), rn = within<DIM, K>(L, dr);
             const bool nl = __any_sync(0xffffffffu, ln), nr = __any_sync(0xffffffffu, rn);
             if (nl && nr && nd.left < 0 && nd.right < 0) {
                 // two leaf children: one contiguous span [start, end) of <= 2 leaves
                 scan_leaves<DIM, K>(recs, ~nd.left, nd.mid, ~nd.right, ln, rn, ps_lo, ps_hi, L, S, lane);
             } else if (nl && nr) {
                 // visit first the child nearer for most lanes (performance only, reading 10)
-                const bool lfirst =
-                    __popc(__ballot_sync(0xffffffffu, box_order<DIM, K>(L, nd.lbox) <= box_order<DIM, K>(L, nd.rbox))) >= 16;
+                const bool lfirst = __popc(__ballot_sync(0xffffffffu, dl <= dr)) >= 16;
                 const Ref far = lfirst ? right_child<DIM>(nd) : left_child<DIM>(nd);
                 __syncwarp();
                 if (lane == 0) {
@@ -541,9 +548,14 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
             const int4 e = S.stk[sp];
             {
                 // the far child's box: right box (side 1) or left box of its parent node
-                const Node<DIM>* pn_node = nodes + e.z;
+                using BT = typename BoxT<DIM>::T;
+                const BT* src = e.w ? nodes[e.z].rbox : nodes[e.z].lbox;   // 8-byte aligned
 #pragma unroll
-                for (int t = 0; t < 2 * DIM; ++t) bx[t] = __ldg(e.w ? &pn_node->rbox[t] : &pn_node->lbox[t]);
+                for (int t = 0; t < DIM; ++t) {
+                    const int2 v = __ldg(reinterpret_cast<const int2*>(src) + t);
+                    bx[2 * t] = *reinterpret_cast<const BT*>(&v.x);
+                    bx[2 * t + 1] = *reinterpret_cast<const BT*>(&v.y);
+                }
             }
             const Ref popped{e.x, e.y};
 #else
