@@ -168,7 +168,7 @@ unsigned long long* d_count(zd_tree* h) { return reinterpret_cast<unsigned long 
 void free_tree_bufs(zd_tree* h) {
     TreeBufs& t = h->tb;
     dfree(t.pt_leaf, h->st); dfree(t.leaf_start, h->st); dfree(t.leaf_parent, h->st);
-    dfree(t.split_bit, h->st); dfree(t.visit, h->st); dfree(t.range, h->st);
+    dfree(t.split_bit, h->st); dfree(t.visit, h->st); dfree(t.range, h->st); dfree(t.pos_range, h->st);
     dfree(t.flags, h->st); dfree(t.block_cnt, h->st);
     if (t.nodes) { cudaFreeAsync(t.nodes, h->st); t.nodes = nullptr; }
 }
@@ -184,6 +184,7 @@ int alloc_tree_bufs(zd_tree* h, int64_t cap) {
     ZD_CUDA(dalloc(&t.split_bit, cap, h->st));
     ZD_CUDA(dalloc(&t.visit, cap, h->st));
     ZD_CUDA(dalloc(&t.range, 2 * cap, h->st));
+    ZD_CUDA(dalloc(&t.pos_range, cap, h->st));
     ZD_CUDA(dalloc(&t.flags, cap, h->st));
     ZD_CUDA(dalloc(&t.block_cnt, std::max(tree_blocks(cap), compact_blocks(cap)) + 2, h->st));
     ZD_CUDA(cudaMallocAsync(&t.nodes, std::max<int64_t>(cap, 1) * node_bytes, h->st));
@@ -458,6 +459,7 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
     a.dim = h->dim; a.k = k; a.n = h->n;
     a.recs = h->recs; a.pt_leaf = h->tb.pt_leaf; a.leaf_start = h->tb.leaf_start;
     a.leaf_parent = h->tb.leaf_parent; a.nodes = h->tb.nodes; a.node_range = h->tb.range;
+    a.pos_range = h->tb.pos_range;
     a.split_bit = h->tb.split_bit;
     a.d_meta = h->d_small;
     a.out_idx = di; a.out_d2 = dd;

@@ -37,6 +37,7 @@ struct TreeBufs {
     void* nodes;           // [cap]   Node<dim>
     uint32_t* visit;       // [cap]   bottom-up arrival counters
     int32_t* range;        // [2*cap] bottom-up leaf-range scratch
+    int2* pos_range;       // [cap]   sorted point range [x, y) of internal node i
     uint8_t* flags;        // [cap]   big-pair flags
     uint32_t* block_cnt;   // [tree_blocks(cap)+1]
     int32_t* d_meta;       // [4]: nb (internal count), root ref
@@ -59,6 +60,7 @@ struct KnnArgs {
     const int32_t* leaf_parent;
     const void* nodes;
     const int32_t* node_range;   // [2*n_internal]: leaves [L, R] under internal node i
+    const int2* pos_range;       // [n_internal]: sorted point range of internal node i
     const int32_t* split_bit;    // [n_internal]
     const int32_t* d_meta;       // root ref at [1]
     const int32_t* row_of_id;    // NULL: row = id

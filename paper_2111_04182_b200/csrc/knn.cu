@@ -162,24 +162,24 @@ struct Cap {   // buffered candidates per lane (overflow compacts per lane: any 
 
 // A child reference in traversal form: ref >= 0 internal node; ref < 0 a leaf with
 // points [~ref, end).
-struct Ref {
-    int32_t ref, end;
-};
-
-template <int DIM>
-__device__ __forceinline__ Ref left_child(const Node<DIM>& nd) { return Ref{nd.left, nd.mid}; }
-template <int DIM>
-__device__ __forceinline__ Ref right_child(const Node<DIM>& nd) {
-    return nd.right >= 0 ? Ref{nd.right, 0} : Ref{~nd.mid, ~nd.right};
-}
-
-struct alignas(16) StkEntry {
-    int4 a, b;          // a = (ref, box words 0..2), b = (box words 3..5, leaf end)
-};
-
-#ifndef ZD_STK16
-#define ZD_STK16 1   // 16-byte stack entries; the far child's box is re-read from its parent
+// A subtree in traversal form with its sorted point range [s, e): ref >= 0 an
+// internal node; ref < 0 a contiguous span scanned directly — a leaf, or (query-side
+// coarsening) a subtree of at most ZD_COARSE points, whose points are contiguous too.
+#ifndef ZD_COARSE
+#define ZD_COARSE 32
 #endif
+struct Ref {
+    int32_t ref, s, e;
+};
+__device__ __forceinline__ Ref child_ref(int32_t c, int32_t s, int32_t e) {
+    return (c < 0 || e - s <= ZD_COARSE) ? Ref{~s, s, e} : Ref{c, s, e};
+}
+template <int DIM>
+__device__ __forceinline__ Ref left_child(const Node<DIM>& nd, int32_t s) { return child_ref(nd.left, s, nd.mid); }
+template <int DIM>
+__device__ __forceinline__ Ref right_child(const Node<DIM>& nd, int32_t e) { return child_ref(nd.right, nd.mid, e); }
+
+
 #ifndef ZD_F32FILTER
 #define ZD_F32FILTER 1   // 3D: candidate tests in fp32 (exact coordinates), confirmed in int64
 #endif
@@ -191,11 +191,7 @@ struct WarpSh {
 #endif
     int32_t bp[Cap<K>::v][32];           // per-lane buffered positions; column = lane
     float bf[Cap<K>::v][32];             //   ... and their d2 rounded up to fp32
-#if ZD_STK16
-    int4 stk[kStk];                      // (ref, leaf end, parent node, side): box reloaded on pop
-#else
-    StkEntry stk[kStk];
-#endif
+    int4 stk[kStk];                      // (ref, s, e, parent | side << 31): box reloaded on pop
 };
 
 template <int DIM, int K>
@@ -469,73 +465,68 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
     }
 }
 
-// scan [s, e) minus the already scanned span [ps_lo, ps_hi) (a union of whole leaves)
+// Scan the spans [s, mid) (lanes with needl) and [mid, e) (lanes with needr; mid == e
+// for a single span) minus the already scanned [ps_lo, ps_hi); a lane that needs
+// either span tests both.  Two adjacent spans are staged together.
 template <int DIM, int K>
 __device__ __forceinline__ void scan_leaves(const int4* __restrict__ recs, int32_t s, int32_t mid, int32_t e,
                                             bool needl, bool needr, int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L,
                                             WarpSh<K>& S, int lane) {
-    // [s, mid) and [mid, e) are whole leaves (mid == e for a single leaf); a lane that
-    // needs either leaf tests both
-    const bool skip_l = s >= ps_lo && s < ps_hi;
-    const bool skip_r = mid < e && mid >= ps_lo && mid < ps_hi;
-    const int32_t a = skip_l ? mid : s, b = skip_r ? mid : e;
-    if (a < b) scan_span<DIM, K>(recs, a, b, (!skip_l && needl) || (!skip_r && needr), L, S, lane);
+    const int32_t a1 = min(e, max(s, ps_lo));   // piece before the scanned span: [s, a1)
+    const int32_t b0 = max(s, min(e, ps_hi));   // piece after it: [b0, e)
+    // one inlined copy of scan_span for both pieces (code size: the I-cache matters)
+#pragma unroll 1
+    for (int pc = 0; pc < 2; ++pc) {
+        const int32_t x0 = pc ? b0 : s, x1 = pc ? e : a1;
+        if (x0 < x1) scan_span<DIM, K>(recs, x0, x1, (needl && x0 < mid) || (needr && x1 > mid), L, S, lane);
+    }
 }
 
-template <int DIM>
-__device__ __forceinline__ void unpack_box(const StkEntry& e, int32_t (&bx)[2 * DIM]) {
-    const int w[6] = {e.a.y, e.a.z, e.a.w, e.b.x, e.b.y, e.b.z};
-#pragma unroll
-    for (int a = 0; a < 2 * DIM; ++a) bx[a] = w[a];
-}
-
-// Joint Alg. 2 over the subtree `cur`; the span [ps_lo, ps_hi) was scanned already.
+// Joint Alg. 2 over the subtree `cur` (needed by the lanes with cur_need); the span
+// [ps_lo, ps_hi) was scanned already.  Far children wait on a per-warp shared-memory
+// stack as (ref, s, e, parent | side << 31); their box is re-read from the parent.
 template <int DIM, int K>
 __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const Node<DIM>* __restrict__ nodes, Ref cur,
                                            bool cur_need, int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L,
                                            WarpSh<K>& S, int lane) {
     int sp = 0;
     while (true) {
-        bool descend = false;
+        bool descend = false, scan = false;
+        int32_t ss = cur.s, sm = cur.e, se = cur.e;   // span(s) to scan: [ss, sm) and [sm, se)
+        bool sl = cur_need, sr = false;
         if (cur.ref < 0) {
-            scan_leaves<DIM, K>(recs, ~cur.ref, cur.end, cur.end, cur_need, false, ps_lo, ps_hi, L, S, lane);
+            scan = true;
         } else {
             ZD_STAT(ZS_NODES, 1);
             const Node<DIM> nd = load_node<DIM>(nodes + cur.ref);
             const typename BoxD<DIM>::T dl = box_dist<DIM, K>(L, nd.lbox), dr = box_dist<DIM, K>(L, nd.rbox);
             const bool ln = within<DIM, K>(L, dl), rn = within<DIM, K>(L, dr);
             const bool nl = __any_sync(0xffffffffu, ln), nr = __any_sync(0xffffffffu, rn);
-            if (nl && nr && nd.left < 0 && nd.right < 0) {
-                // two leaf children: one contiguous span [start, end) of <= 2 leaves
-                scan_leaves<DIM, K>(recs, ~nd.left, nd.mid, ~nd.right, ln, rn, ps_lo, ps_hi, L, S, lane);
+            const Ref lc = left_child<DIM>(nd, cur.s), rc = right_child<DIM>(nd, cur.e);
+            if (nl && nr && lc.ref < 0 && rc.ref < 0) {
+                // two spans (leaves or small subtrees): adjacent point ranges, one scan
+                scan = true;
+                sm = nd.mid;
+                sl = ln;
+                sr = rn;
             } else if (nl && nr) {
                 // visit first the child nearer for most lanes (performance only, reading 10)
                 const bool lfirst = __popc(__ballot_sync(0xffffffffu, dl <= dr)) >= 16;
-                const Ref far = lfirst ? right_child<DIM>(nd) : left_child<DIM>(nd);
+                const Ref far = lfirst ? rc : lc;
                 __syncwarp();
-                if (lane == 0) {
-#if ZD_STK16
-                    S.stk[sp] = make_int4(far.ref, far.end, cur.ref, lfirst ? 1 : 0);
-#else
-                    int w6[6] = {0, 0, 0, 0, 0, 0};
-#pragma unroll
-                    for (int a = 0; a < 2 * DIM; ++a) w6[a] = lfirst ? nd.rbox[a] : nd.lbox[a];
-                    StkEntry e;
-                    e.a = make_int4(far.ref, w6[0], w6[1], w6[2]);
-                    e.b = make_int4(w6[3], w6[4], w6[5], far.end);
-                    S.stk[sp] = e;
-#endif
-                }
+                if (lane == 0)
+                    S.stk[sp] = make_int4(far.ref, far.s, far.e, (int32_t)((uint32_t)cur.ref | (lfirst ? 0x80000000u : 0u)));
                 ++sp;
-                cur = lfirst ? left_child<DIM>(nd) : right_child<DIM>(nd);
+                cur = lfirst ? lc : rc;
                 cur_need = lfirst ? ln : rn;
                 descend = true;
             } else if (nl || nr) {
-                cur = nl ? left_child<DIM>(nd) : right_child<DIM>(nd);
+                cur = nl ? lc : rc;
                 cur_need = nl ? ln : rn;
                 descend = true;
             }
         }
+        if (scan) scan_leaves<DIM, K>(recs, ss, sm, se, sl, sr, ps_lo, ps_hi, L, S, lane);
         if (descend) continue;
         // pop the next far child that some lane still needs
         bool found = false;
@@ -543,13 +534,13 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
         while (sp > 0) {
             --sp;
             ZD_STAT(ZS_POPS, 1);
-            typename BoxT<DIM>::T bx[2 * DIM];
-#if ZD_STK16
             const int4 e = S.stk[sp];
+            typename BoxT<DIM>::T bx[2 * DIM];
             {
-                // the far child's box: right box (side 1) or left box of its parent node
+                // the far child's box: right box (side bit set) or left box of its parent
                 using BT = typename BoxT<DIM>::T;
-                const BT* src = e.w ? nodes[e.z].rbox : nodes[e.z].lbox;   // 8-byte aligned
+                const Node<DIM>* pnode = nodes + (e.w & 0x7fffffff);
+                const BT* src = (e.w < 0) ? pnode->rbox : pnode->lbox;   // 8-byte aligned
 #pragma unroll
                 for (int t = 0; t < DIM; ++t) {
                     const int2 v = __ldg(reinterpret_cast<const int2*>(src) + t);
@@ -557,20 +548,9 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
                     bx[2 * t + 1] = *reinterpret_cast<const BT*>(&v.y);
                 }
             }
-            const Ref popped{e.x, e.y};
-#else
-            const StkEntry e = S.stk[sp];
-            {
-                int32_t bi[2 * DIM];
-                unpack_box<DIM>(e, bi);
-#pragma unroll
-                for (int t = 0; t < 2 * DIM; ++t) bx[t] = (typename BoxT<DIM>::T)bi[t];
-            }
-            const Ref popped{e.a.x, e.b.w};
-#endif
-            const bool pn = box_need<DIM, K>(L, bx);
+            const bool pn = within<DIM, K>(L, box_dist<DIM, K>(L, bx));
             if (__any_sync(0xffffffffu, pn)) {
-                cur = popped;
+                cur = Ref{e.x, e.y, e.z};
                 cur_need = pn;
                 found = true;
                 break;
@@ -587,6 +567,7 @@ struct PacketArgs {
     const void* nodes;
     const int32_t* node_range;
     const int32_t* split_bit;  // per internal node (in-order)
+    const int2* pos_range;     // per internal node: sorted point range [x, y)
     const int4* qrecs;         // queries in Morton order: (x, y, z|0, id or query index)
     const int32_t* qleaf;      // leaf of each query
     int32_t nq;
@@ -701,7 +682,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
 
     // C = the node whose subtree has been searched (-1: the single leaf lA)
     int32_t C = -1, P;
-    Ref sub{kNoSub, 0};
+    Ref sub{kNoSub, 0, 0};
     bool sub_need = active;
     if (lA == lB) {
         P = __ldg(A.leaf_parent + lA);
@@ -722,7 +703,8 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         }
         C = x;
         P = __ldg(&nodes[x].parent);
-        sub = Ref{x, 0};
+        const int2 xr = __ldg(A.pos_range + x);
+        sub = child_ref(x, xr.x, xr.y);
     }
     while (true) {
         if (sub.ref != kNoSub) joint_down<DIM, K>(A.recs, nodes, sub, sub_need, ps_lo, ps_hi, L, S, lane);
@@ -738,8 +720,13 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         }
         if (__all_sync(0xffffffffu, lane_stop<DIM, K>(L, cb))) break;
         sub_need = box_need<DIM, K>(L, sb);
-        sub = __any_sync(0xffffffffu, sub_need) ? (isl ? right_child<DIM>(nd) : left_child<DIM>(nd))
-                                                              : Ref{kNoSub, 0};
+        if (__any_sync(0xffffffffu, sub_need)) {
+            // the sibling's point range: [mid, end of P) or [start of P, mid)
+            const int2 pr = __ldg(A.pos_range + P);
+            sub = isl ? right_child<DIM>(nd, pr.y) : left_child<DIM>(nd, pr.x);
+        } else {
+            sub = Ref{kNoSub, 0, 0};
+        }
         C = P;
         P = nd.parent;
     }
@@ -828,7 +815,7 @@ __global__ void __launch_bounds__(256) locate_kernel(const uint64_t* __restrict_
 PacketArgs packet_args(const KnnArgs& a) {
     PacketArgs A{};
     A.recs = a.recs; A.leaf_start = a.leaf_start; A.leaf_parent = a.leaf_parent;
-    A.nodes = a.nodes; A.node_range = a.node_range; A.split_bit = a.split_bit;
+    A.nodes = a.nodes; A.node_range = a.node_range; A.split_bit = a.split_bit; A.pos_range = a.pos_range;
     A.k = a.k; A.row_of_id = a.row_of_id; A.out_idx = a.out_idx; A.out_d2 = a.out_d2;
     A.hard_list = a.hard_list; A.hard_count = a.hard_count; A.hard_cap = a.hard_cap; A.hard_mode = 0;
     A.defer_all = a.defer_all;

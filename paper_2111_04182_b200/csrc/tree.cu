@@ -128,7 +128,7 @@ template <int DIM>
 __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__ recs, const int32_t* __restrict__ leaf_start,
                                                         const int32_t* __restrict__ split_bit, int32_t* meta,
                                                         Node<DIM>* nodes, int32_t* __restrict__ leaf_parent,
-                                                        uint32_t* visit, int32_t* range) {
+                                                        uint32_t* visit, int32_t* range, int2* __restrict__ pos_range) {
     const int32_t nb = meta[0];
     for (int32_t l = blockIdx.x * blockDim.x + threadIdx.x; l <= nb; l += gridDim.x * blockDim.x) {
         // leaf box from its records
@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__
                 bb[DIM + a] = max(bb[DIM + a], (int32_t)__ldcg(sb + DIM + a));
             }
             if (as_right) L = __ldcg(range + 2 * par); else R = __ldcg(range + 2 * par + 1);
+            pos_range[par] = make_int2(__ldg(leaf_start + L), __ldg(leaf_start + R + 1));
             ref = par;
             if (L == 0 && R == nb) { P->parent = -1; meta[1] = par; break; }
         }
@@ -233,10 +234,10 @@ void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, 
     count_launch(1);
     if (dim == 2)
         bottom_up_kernel<2><<<grid, 128, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<2>*)t.nodes,
-                                                  t.leaf_parent, t.visit, t.range);
+                                                  t.leaf_parent, t.visit, t.range, t.pos_range);
     else
         bottom_up_kernel<3><<<grid, 128, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<3>*)t.nodes,
-                                                  t.leaf_parent, t.visit, t.range);
+                                                  t.leaf_parent, t.visit, t.range, t.pos_range);
 }
 
 }  // namespace zd

@@ -23,6 +23,8 @@ def build():
     from concurrent.futures import ThreadPoolExecutor
     out = ROOT / "build_var"
     out.mkdir(exist_ok=True)
+    for old in out.glob("*.so"):   # only the current variants travel to the GPU box
+        old.unlink()
     with ThreadPoolExecutor(4) as ex:
         list(ex.map(lambda kv: zd.build_lib(force=True, defines=kv[1], out=out / f"{kv[0]}.so"), VARIANTS.items()))
 
