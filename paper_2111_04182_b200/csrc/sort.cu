@@ -124,14 +124,17 @@ __global__ void __launch_bounds__(ST) onesweep_kernel(
     const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
     for (int j = 0; j < SI; ++j) {
-        uint32_t d = (uint32_t)(key[j] >> shift) & 255u;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
-        uint32_t lower = __popc(peers & lt_mask);
-        uint32_t old = u.hist[w][d];
-        __syncwarp();
-        if (lower == 0) u.hist[w][d] = old + __popc(peers);
-        __syncwarp();
-        loc[j] = old + lower;
+        // the lowest lane of each digit group bumps the warp-private counter by the
+        // group size (shared-memory atomic: same-address atomics of one warp are
+        // applied in issue order, so key j's group precedes key j+1's — stable) and
+        // broadcasts the old value; no __syncwarp chain between the SI keys
+        const uint32_t d = (uint32_t)(key[j] >> shift) & 255u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (lane == leader) old = atomicAdd(&u.hist[w][d], (uint32_t)__popc(peers));
+        old = __shfl_sync(0xffffffffu, old, leader);
+        loc[j] = old + __popc(peers & lt_mask);
     }
     __syncthreads();
 
