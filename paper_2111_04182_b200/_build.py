@@ -39,7 +39,7 @@ def stale(path: Path = LIB_PATH) -> bool:
 
 def build_lib(force: bool = False, verbose: bool = False, stats: bool = False, defines=(), out=None) -> Path:
     """Build libzd.so (or, for experiments, a variant with extra -D defines at `out`)."""
-    path = Path(out) if out else (STATS_LIB_PATH if stats else LIB_PATH)
+    path = Path(out).resolve() if out else (STATS_LIB_PATH if stats else LIB_PATH)
     if not force and not stale(path):
         return path
     tmp = path.with_name(f"{path.name}.tmp{os.getpid()}")

@@ -6,6 +6,17 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Device-side bounds assertions for the debug build (-DZD_DEBUG; tests load it via
+// ZD_LIB=<path>): the substitute for compute-sanitizer, which is unavailable here.
+#ifdef ZD_DEBUG
+#include <cassert>
+#define ZD_DCHECK(c) assert(c)
+#else
+#define ZD_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 namespace zd {
 
 constexpr int kWarp = 32;

@@ -192,6 +192,9 @@ struct WarpSh {
     int32_t bp[Cap<K>::v][32];           // per-lane buffered positions; column = lane
     float bf[Cap<K>::v][32];             //   ... and their d2 rounded up to fp32
     int4 stk[kStk];                      // (ref, s, e, parent | side << 31): box reloaded on pop
+#ifdef ZD_DEBUG
+    int32_t dbg_npts, dbg_nint;          // bounds for ZD_DCHECK
+#endif
 };
 
 template <int DIM, int K>
@@ -334,6 +337,9 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
         const int n32 = min(32, e - b);
         __syncwarp();
         if (lane < n32) {
+#ifdef ZD_DEBUG
+            ZD_DCHECK(b >= 0 && b + lane < S.dbg_npts);
+#endif
             const int4 r = __ldg(recs + b + lane);
             S.c[lane] = r;
 #if ZD_F32FILTER
@@ -457,6 +463,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                         compact<DIM, K>(L, S, lane);
                     }
                 }
+                ZD_DCHECK(L.cnt < Cap<K>::v);
                 S.bp[L.cnt][lane] = b + j;
                 S.bf[L.cnt][lane] = xf;
                 ++L.cnt;
@@ -498,6 +505,9 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
             scan = true;
         } else {
             ZD_STAT(ZS_NODES, 1);
+#ifdef ZD_DEBUG
+            ZD_DCHECK(cur.ref < S.dbg_nint && cur.s < cur.e && cur.e <= S.dbg_npts);
+#endif
             const Node<DIM> nd = load_node<DIM>(nodes + cur.ref);
             const typename BoxD<DIM>::T dl = box_dist<DIM, K>(L, nd.lbox), dr = box_dist<DIM, K>(L, nd.rbox);
             const bool ln = within<DIM, K>(L, dl), rn = within<DIM, K>(L, dr);
@@ -514,6 +524,7 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
                 const bool lfirst = __popc(__ballot_sync(0xffffffffu, dl <= dr)) >= 16;
                 const Ref far = lfirst ? rc : lc;
                 __syncwarp();
+                ZD_DCHECK(sp < kStk);
                 if (lane == 0)
                     S.stk[sp] = make_int4(far.ref, far.s, far.e, (int32_t)((uint32_t)cur.ref | (lfirst ? 0x80000000u : 0u)));
                 ++sp;
@@ -571,6 +582,8 @@ struct PacketArgs {
     const int4* qrecs;         // queries in Morton order: (x, y, z|0, id or query index)
     const int32_t* qleaf;      // leaf of each query
     int32_t nq;
+    int32_t n_pts;             // tree points (bounds checks)
+    const int32_t* d_meta;     // [0] = internal node count (bounds checks)
     int k;
     const int32_t* row_of_id;  // all-points: row of an id (NULL: row = id)
     int32_t* out_idx;
@@ -710,6 +723,9 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         if (sub.ref != kNoSub) joint_down<DIM, K>(A.recs, nodes, sub, sub_need, ps_lo, ps_hi, L, S, lane);
         if (P < 0) break;
         ZD_STAT(ZS_ASCENTS, 1);
+#ifdef ZD_DEBUG
+        ZD_DCHECK(P < S.dbg_nint);
+#endif
         const Node<DIM> nd = load_node<DIM>(nodes + P);
         const bool isl = C >= 0 ? nd.left == C : P == lA;   // leaf l is the left child of node l
         typename BoxT<DIM>::T cb[2 * DIM], sb[2 * DIM];
@@ -775,6 +791,13 @@ __global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? ZD_MINB : 2)) knn_pa
     WarpSh<K>* sh = reinterpret_cast<WarpSh<K>*>(smem_raw);   // Pw<K>::v warps
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSh<K>& S = sh[wib];
+#ifdef ZD_DEBUG
+    if (lane == 0) {
+        S.dbg_nint = __ldg(A.d_meta);
+        S.dbg_npts = A.n_pts;
+    }
+    __syncwarp();
+#endif
     const int64_t gw = (int64_t)blockIdx.x * Pw<K>::v + wib;
     if (!A.hard_mode) {
         const int64_t p0 = gw * 32;
@@ -816,6 +839,7 @@ PacketArgs packet_args(const KnnArgs& a) {
     PacketArgs A{};
     A.recs = a.recs; A.leaf_start = a.leaf_start; A.leaf_parent = a.leaf_parent;
     A.nodes = a.nodes; A.node_range = a.node_range; A.split_bit = a.split_bit; A.pos_range = a.pos_range;
+    A.n_pts = (int32_t)a.n; A.d_meta = a.d_meta;
     A.k = a.k; A.row_of_id = a.row_of_id; A.out_idx = a.out_idx; A.out_d2 = a.out_d2;
     A.hard_list = a.hard_list; A.hard_count = a.hard_count; A.hard_cap = a.hard_cap; A.hard_mode = 0;
     A.defer_all = a.defer_all;

@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(ST) onesweep_kernel(
         uint64_t k = u.keys[i];
         uint32_t d = (uint32_t)(k >> shift) & 255u;
         uint32_t dest = s_glob[d] + i;
+        ZD_DCHECK(dest < n);
         keys_out[dest] = k;
         if (MODE == 2) recs_out[dest] = decode_rec<DIM>(k, (int)s_ids[i]);
         else ids_out[dest] = s_ids[i];

@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__
             else if (R == nb) { par = L - 1; as_right = true; }
             else if (__ldg(split_bit + L - 1) < __ldg(split_bit + R)) { par = L - 1; as_right = true; }
             else { par = R; as_right = false; }
+            ZD_DCHECK(par >= 0 && par < nb && L >= 0 && R <= nb);
             Node<DIM>* P = nodes + par;
             // a leaf child is encoded by its point range: left = ~start, right = ~end
             const int32_t cref = ref >= 0 ? ref : (as_right ? ~e : ~s);

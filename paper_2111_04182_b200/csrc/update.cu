@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(MT) merge_kernel(const uint64_t* __restrict__ 
     __syncthreads();
     for (int o = threadIdx.x; o < na + nb; o += MT) {
         const int sidx = s_src[o];
+        ZD_DCHECK(d0 + o < tot && (sidx >= 0 ? sidx < na : ~sidx < nb));
         ko[d0 + o] = sidx >= 0 ? s_key[sidx] : s_key[na + ~sidx];
         ro[d0 + o] = sidx >= 0 ? __ldg(ra + a0 + sidx) : __ldg(rb + b0 + ~sidx);
     }
@@ -188,6 +189,7 @@ __global__ void __launch_bounds__(CT) compact_write_kernel(const uint32_t* __res
     for (int j = 0; j < CPI; ++j) {
         if ((bal[j] >> lane) & 1u) {
             const uint32_t o = off + s_cnt[j * NW + w] + __popc(bal[j] & lt);
+            ZD_DCHECK(o < n);
             ko[o] = __ldg(ki + base + (int64_t)j * CT);
             ro[o] = r[j];
         }
