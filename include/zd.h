@@ -100,6 +100,15 @@ ZD_API zd_tree *zd_build_ex(const int32_t *points, int64_t n, int dim, const zd_
 ZD_API int zd_knn(zd_tree *h, const int32_t *queries, int64_t m, int k,
            int32_t *out_idx, int64_t *out_dist2);
 
+/* zd_knn with options.  flags: 0 = zd_knn (leaf-based search: every query
+ * starts at its own leaf and ascends, Alg. 3); ZD_KNN_ROOT_BASED = the
+ * root-based variant (Alg. 2 from the root with an empty neighbour list), kept
+ * as an ablation — the answer is identical, the work differs (the paper's Fig. 2).
+ * Unknown flags -> ZD_EINVAL. */
+#define ZD_KNN_ROOT_BASED 1
+ZD_API int zd_knn_ex(zd_tree *h, const int32_t *queries, int64_t m, int k,
+              int32_t *out_idx, int64_t *out_dist2, int flags);
+
 /* Insert m points (int32 [m][dim]); they get ids first, first+1, ... where
  * first = the next unused id (ids are never reused, reading 20).  Returns first
  * (>= 0) or a negative code; on error the tree is unchanged.  The tree after the

@@ -23,6 +23,7 @@ from ._build import LIB_PATH, STATS_LIB_PATH, build_lib
 
 ZD_OK, ZD_EINVAL, ZD_ERANGE, ZD_ENOMEM, ZD_ECUDA = 0, -1, -2, -3, -4
 ZD_K_MAX = 32
+ZD_KNN_ROOT_BASED = 1
 ZD_LEAF_MAX_MAX = 32
 PHASES = ("sort", "topology", "bbox", "merge_compact", "knn", "validate")
 
@@ -63,6 +64,8 @@ def load():
     L.zd_build_ex.argtypes = [P, i64, i32, C.POINTER(_Opts)]
     L.zd_knn.restype = i32
     L.zd_knn.argtypes = [P, P, i64, i32, P, P]
+    L.zd_knn_ex.restype = i32
+    L.zd_knn_ex.argtypes = [P, P, i64, i32, P, P, i32]
     L.zd_insert.restype = i64
     L.zd_insert.argtypes = [P, P, i64]
     L.zd_delete.restype = i64
@@ -165,10 +168,11 @@ class ZdTree:
         return self._h
 
     # -- queries
-    def zd_knn(self, k: int, queries=None, out_idx=None, out_dist2=None, device=None):
+    def zd_knn(self, k: int, queries=None, out_idx=None, out_dist2=None, device=None, root_based: bool = False):
         """Exact k-NN.  queries=None: all live points (rows by ascending live id).
         Returns (out_idx int32 [m,k], out_dist2 int64 [m,k]); allocated on `device`
-        (default: cuda) when not given."""
+        (default: cuda) when not given.  root_based=True: the root-based search
+        variant (zd_knn_ex, ZD_KNN_ROOT_BASED), same answer."""
         import torch
         q = None if queries is None else _as_i32(queries)
         m = self.zd_size() if q is None else int(q.shape[0])
@@ -176,7 +180,10 @@ class ZdTree:
             dev = device or "cuda"
             out_idx = torch.empty((m, k), dtype=torch.int32, device=dev)
             out_dist2 = torch.empty((m, k), dtype=torch.int64, device=dev)
-        _check(load().zd_knn(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2)))
+        if root_based:
+            _check(load().zd_knn_ex(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2), ZD_KNN_ROOT_BASED))
+        else:
+            _check(load().zd_knn(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2)))
         return out_idx, out_dist2
 
     def zd_insert(self, batch) -> int:

@@ -70,6 +70,7 @@ struct KnnArgs {
     int32_t* hard_count;         // zeroed by the caller
     int hard_cap;
     int defer_all;               // testing: every packet goes to the second pass
+    int root_based;              // ablation: root-based search
 };
 int knn_kmax();
 // Work counters of the packet k-NN kernel (only in a -DZD_KNN_STATS build).

@@ -593,6 +593,7 @@ struct PacketArgs {
     int hard_cap;
     int hard_mode;             // 0: packets; 1: second pass over the deferred packets' queries
     int defer_all;             // testing: defer every packet (hard_list must be set)
+    int root_based;            // ablation: root-based search instead of leaf-based
 };
 
 #ifndef ZD_INCOHERENT
@@ -645,10 +646,13 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         }
         if (lB - lA > 8) lB = lA;
     }
-    const int32_t ps_lo = __ldg(A.leaf_start + lA), ps_hi = __ldg(A.leaf_start + lB + 1);
-    scan_span<DIM, K>(A.recs, ps_lo, ps_hi, active, L, S, lane);
+    // root-based search (ablation): Alg. 2 from the root with an empty list, no
+    // leaf seed and no ascent; leaf-based (default): seed with the packet's leaves
+    const int32_t ps_lo = A.root_based ? 0 : __ldg(A.leaf_start + lA);
+    const int32_t ps_hi = A.root_based ? 0 : __ldg(A.leaf_start + lB + 1);
+    if (!A.root_based) scan_span<DIM, K>(A.recs, ps_lo, ps_hi, active, L, S, lane);
 
-    if (can_defer) {
+    if (can_defer && !A.root_based) {
         // A packet whose queries are far apart compared with their neighbour distances
         // (32 Morton-consecutive points straddling a large Morton-cell boundary) would
         // make one warp search several distant regions jointly; it is deferred to a
@@ -697,7 +701,11 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
     int32_t C = -1, P;
     Ref sub{kNoSub, 0, 0};
     bool sub_need = active;
-    if (lA == lB) {
+    if (A.root_based) {
+        const int32_t root = __ldg(A.d_meta + 1);   // internal index, or ~0 for a single leaf
+        sub = root >= 0 ? child_ref(root, 0, A.n_pts) : Ref{~0, 0, A.n_pts};
+        P = -1;
+    } else if (lA == lB) {
         P = __ldg(A.leaf_parent + lA);
     } else {
         // lowest common ancestor of leaves lA < lB = the separator node in [lA, lB)
@@ -843,6 +851,7 @@ PacketArgs packet_args(const KnnArgs& a) {
     A.k = a.k; A.row_of_id = a.row_of_id; A.out_idx = a.out_idx; A.out_d2 = a.out_d2;
     A.hard_list = a.hard_list; A.hard_count = a.hard_count; A.hard_cap = a.hard_cap; A.hard_mode = 0;
     A.defer_all = a.defer_all;
+    A.root_based = a.root_based;
     return A;
 }
 

@@ -296,3 +296,20 @@ def test_knn_deferral_modes(zd, oracle_mod, monkeypatch, mode, dist, dim):
     torch.cuda.synchronize()
     oqi, oqd, _ = oracle_mod.Tree(pts).knn_queries(q, 10)
     check_rows(qi.cpu().numpy(), qd.cpu().numpy(), oqi, oqd)
+
+
+@pytest.mark.parametrize("dist,dim", [("uniform", 2), ("uniform", 3), ("plummer", 3), ("sphere", 3), ("dup", 3)])
+def test_knn_root_based(zd, oracle_mod, dist, dim):
+    """Root-based search (zd_knn_ex ZD_KNN_ROOT_BASED) gives the same unique
+    answer as the leaf-based search and the oracle, all-points and external queries."""
+    pts = zdgen.points(dist, 9000, dim, seed=31)
+    t = zd.zd_build(dev(pts))
+    gi, gd = t.zd_knn(10, root_based=True)
+    torch.cuda.synchronize()
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(10, root_based=True)
+    check_rows(gi.cpu().numpy(), gd.cpu().numpy(), oi, od)
+    q = zdgen.uniform(2000, dim, seed=32)
+    qi, qd = t.zd_knn(10, queries=dev(q), root_based=True)
+    torch.cuda.synchronize()
+    oqi, oqd, _ = oracle_mod.Tree(pts).knn_queries(q, 10)
+    check_rows(qi.cpu().numpy(), qd.cpu().numpy(), oqi, oqd)
