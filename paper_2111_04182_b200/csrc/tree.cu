@@ -43,9 +43,28 @@ __device__ __forceinline__ int delta_of(uint64_t a, uint64_t b) {
     return x ? 63 - __clzll((long long)x) : -1;
 }
 
+// 16-bit mask of the bytes s[p .. p+15] that are > d (signed int8, d >= 0), from
+// word loads of shared memory, funnel shifts and SIMD byte compares.
+__device__ __forceinline__ uint32_t greater_mask16(const int8_t* s, int p, int d) {
+    const int a = p & ~3, sh = (p & 3) * 8;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(s + a);
+    uint32_t words[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) words[i] = w[i];
+    const uint32_t dd = (uint32_t)d * 0x01010101u;
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t v = __funnelshift_r(words[i], words[i + 1], sh);
+        const uint32_t g = __vcmpgts4(v, dd) & 0x80808080u;       // 0x80 in each greater byte
+        m |= ((g * 0x00204081u) >> 28) << (4 * i);                 // byte sign bits -> 4 bits
+    }
+    return m;
+}
+
 __global__ void __launch_bounds__(TT) flags_kernel(const uint64_t* __restrict__ keys, uint32_t n, int leaf_max,
                                                    uint8_t* __restrict__ flags, uint32_t* __restrict__ block_cnt) {
-    __shared__ int8_t s_delta[TTILE + 2 * HALO];
+    __shared__ __align__(16) int8_t s_delta[TTILE + 2 * HALO + 8];
     __shared__ uint32_t s_warp[32];
     const int64_t base = (int64_t)blockIdx.x * TTILE;
     const int64_t npairs = (int64_t)n - 1;
@@ -67,8 +86,19 @@ __global__ void __launch_bounds__(TT) flags_kernel(const uint64_t* __restrict__ 
         bool big = false;
         if (d >= 0) {
             int l = 1, r = 1;
-            while (l <= W && s_delta[c - l] <= d) ++l;
-            while (r <= W && s_delta[c + r] <= d) ++r;
+            if (W <= 15) {
+                // branch-free: nearest larger delta within 16 bytes on each side via
+                // SIMD byte compares (bit k of gl: byte c-16+k > d; of gr: byte c+1+k > d)
+                const uint32_t gl = greater_mask16(s_delta, c - 16, d);
+                const uint32_t gr = greater_mask16(s_delta, c + 1, d);
+                const uint32_t ml = gl & (0xffffu << (16 - W));   // positions c-W .. c-1
+                const uint32_t mr = gr & ((1u << W) - 1u);         // positions c+1 .. c+W
+                l = ml ? 16 - (31 - __clz(ml)) : W + 1;
+                r = mr ? __ffs(mr) : W + 1;
+            } else {
+                while (l <= W && s_delta[c - l] <= d) ++l;
+                while (r <= W && s_delta[c + r] <= d) ++r;
+            }
             big = (l + r) > leaf_max;   // node size = l + r
         }
         flags[p] = big;
