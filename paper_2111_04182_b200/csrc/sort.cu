@@ -154,15 +154,37 @@ __global__ void __launch_bounds__(ST) onesweep_kernel(
     s_start[tid] = start;
 
     // ---- decoupled look-back (one digit per thread)
+    // Windowed: LB predecessors' status words are loaded at once (independent loads,
+    // one round trip) and folded nearest-first until an inclusive prefix; an
+    // unpublished predecessor ends the window and is re-read.  Tile 0 is inclusive,
+    // so the walk never passes it.
     uint32_t excl = 0;
     if (tile > 0) {
-        const uint32_t* p = status + (size_t)(tile - 1) * 256 + tid;
+        constexpr int LB = 8;
+        int64_t t = (int64_t)tile - 1;
         while (true) {
-            uint32_t v = ld_relaxed(p);
-            if ((v & ~VAL_MASK) == 0) continue;   // predecessor not published yet
-            excl += v & VAL_MASK;
-            if ((v & ~VAL_MASK) == FLAG_INC) break;
-            p -= 256;
+            // spin on the nearest unread predecessor alone, then fold a window
+            uint32_t v0;
+            do { v0 = ld_relaxed(status + (size_t)t * 256 + tid); } while ((v0 & ~VAL_MASK) == 0);
+            excl += v0 & VAL_MASK;
+            if ((v0 & ~VAL_MASK) == FLAG_INC) break;
+            --t;
+            uint32_t v[LB];
+#pragma unroll
+            for (int k = 0; k < LB; ++k)
+                v[k] = (t - k >= 0) ? ld_relaxed(status + (size_t)(t - k) * 256 + tid) : (FLAG_INC | 0u);
+            bool done = false;
+            int used = 0;
+#pragma unroll
+            for (int k = 0; k < LB; ++k) {
+                if (done || used < k) continue;                    // stopped earlier in this window
+                if ((v[k] & ~VAL_MASK) == 0) continue;             // not published: spin on it next
+                excl += v[k] & VAL_MASK;
+                used = k + 1;
+                if ((v[k] & ~VAL_MASK) == FLAG_INC) done = true;
+            }
+            if (done) break;
+            t -= used;
         }
         st_relaxed(my_status, FLAG_INC | (excl + cnt));
     }
