@@ -29,7 +29,7 @@ def timed(t, k, root, n, reps=3):
 
 
 def main():
-    configs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C3", "C4a", "C4b", "C2"]
+    configs = sys.argv[1].split(",") if len(sys.argv) > 1 else ["C3", "C4a", "C4b", "C2", "K2"]
     ks = [1, 4, 8, 10, 16, 32]
     for name in configs:
         pts = torch.from_numpy(zdgen.config_points(name)).cuda()

@@ -51,7 +51,7 @@ def test_structure_distributions(zd, oracle_mod, dist, dim, leaf_max):
 
 
 @pytest.mark.parametrize("dist,dim", [("uniform", 2), ("uniform", 3), ("plummer", 3), ("sphere", 3),
-                                      ("dup", 2), ("dup", 3)])
+                                      ("kuzmin", 2), ("dup", 2), ("dup", 3)])
 @pytest.mark.parametrize("k", [1, 3, 5, 10, 16, 32])
 def test_knn_all_distributions(zd, oracle_mod, dist, dim, k):
     pts = zdgen.points(dist, 20000, dim, seed=11)

@@ -246,7 +246,7 @@ def test_knn_golden(oracle_mod):
             assert od[ex["query"]].tolist() == ex["d2"], ex["cite"]
 
 
-CASES = [("uniform", 2, 3000), ("uniform", 3, 3000), ("plummer", 3, 3000), ("sphere", 3, 3000),
+CASES = [("uniform", 2, 3000), ("uniform", 3, 3000), ("plummer", 3, 3000), ("sphere", 3, 3000), ("kuzmin", 2, 3000),
          ("dup", 3, 2000), ("dup", 2, 2000)]
 
 

@@ -47,3 +47,16 @@ def test_delete_ids():
     assert d.min() >= 0 and d.max() < 100_000
     h = zdgen.words(8, np.arange(100_000), 0)
     assert h[d].max() < np.delete(h, d).min()
+
+
+def test_kuzmin_radial_cdf():
+    """Kuzmin disk: M(<R) = 1 - 1/sqrt(1 + R^2), truncated at R = 100."""
+    p = zdgen.kuzmin(200_000, 9).astype(np.float64)
+    assert p.shape == (200_000, 2) and p.min() >= 0 and p.max() < 2 ** 30
+    c = (p + 0.5) / 2 ** 30 * 200.0 - 100.0
+    R = np.sqrt((c ** 2).sum(1))
+    mcut = 1 - 1 / np.sqrt(1 + 100.0 ** 2)
+    for r0 in (0.5, 1.0, 3.0, 10.0):
+        expect = (1 - 1 / np.sqrt(1 + r0 ** 2)) / mcut
+        assert abs((R < r0).mean() - expect) < 0.01, (r0, (R < r0).mean(), expect)
+    assert np.array_equal(zdgen.kuzmin(1000, 9), zdgen.kuzmin(5000, 9)[:1000])

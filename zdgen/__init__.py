@@ -19,6 +19,8 @@ Distributions (PAPER.md P:1212 names them; the grid mapping is ours):
                grid = min(2^21-1, floor((x + 50)/100 * 2^21))      (C4a)
   sphere     : unit sphere (z = 2v-1, phi = 2*pi*w);
                grid = min(2^21-1, floor((x + 1) * 2^20))          (C4b)
+  kuzmin     : 2D Kuzmin disk, R = sqrt((1-u)^-2 - 1), reject R > 100, angle 2*pi*w;
+               grid = min(2^30-1, floor((x + 100)/200 * 2^30))    (paper's 5th set)
   delete ids : the m ids in [0, n) with the smallest (mix64(seed, id), id)
 """
 from __future__ import annotations
@@ -124,6 +126,37 @@ def sphere(n: int, seed: int) -> np.ndarray:
     return out
 
 
+def kuzmin(n: int, seed: int, rmax: float = 100.0) -> np.ndarray:
+    """n x 2 int32 points of a Kuzmin disk (the paper's 2DKuzmin), surface
+    density proportional to (1 + R^2)^(-3/2): M(<R) = 1 - 1/sqrt(1 + R^2), so
+    R = sqrt((1 - u)^(-2) - 1) for u in (0,1) open; reject + redraw R > rmax; angle
+    phi = 2*pi*w; grid = min(2^30-1, floor((x + rmax)/(2 rmax) * 2^30)) per axis."""
+    idx = np.arange(n, dtype=np.uint64)
+    r = np.full(n, np.nan)
+    ww = np.empty(n)
+    todo = np.arange(n)
+    attempt = 0
+    while todo.size:
+        if 2 * attempt + 1 >= DRAWS_PER_POINT:
+            raise RuntimeError("kuzmin: rejection budget exhausted")
+        ii = idx[todo]
+        u = _unit_open(words(seed, ii, 2 * attempt))
+        w = _unit(words(seed, ii, 2 * attempt + 1))
+        rr = np.sqrt((1.0 - u) ** -2.0 - 1.0)
+        ok = rr <= rmax
+        sel = todo[ok]
+        r[sel], ww[sel] = rr[ok], w[ok]
+        todo = todo[~ok]
+        attempt += 1
+    phi = 2.0 * np.pi * ww
+    out = np.empty((n, 2), dtype=np.int32)
+    scale = float(1 << B2)
+    for a, c in enumerate((r * np.cos(phi), r * np.sin(phi))):
+        g = np.floor((c + rmax) / (2.0 * rmax) * scale)
+        out[:, a] = np.clip(g, 0, (1 << B2) - 1).astype(np.int32)
+    return out
+
+
 def delete_ids(n: int, m: int, seed: int) -> np.ndarray:
     """The m ids of [0, n) with the smallest (mix64 word, id); int32, ascending id."""
     if m >= n:
@@ -166,6 +199,7 @@ CONFIGS = {
     "C3": dict(dim=3, n=10_000_000, dist="uniform", seed=3),
     "C4a": dict(dim=3, n=10_000_000, dist="plummer", seed=4),
     "C4b": dict(dim=3, n=10_000_000, dist="sphere", seed=5),
+    "K2": dict(dim=2, n=10_000_000, dist="kuzmin", seed=9),   # not a BASELINE config: P:1212's 2DKuzmin
     "C5": dict(dim=3, n=10_000_000, dist="uniform", seed=6,
                insert_m=1_000_000, insert_seed=7, delete_m=1_000_000, delete_seed=8),
 }
@@ -180,6 +214,9 @@ def points(dist: str, n: int, dim: int, seed: int) -> np.ndarray:
     if dist == "sphere":
         assert dim == 3
         return sphere(n, seed)
+    if dist == "kuzmin":
+        assert dim == 2
+        return kuzmin(n, seed)
     if dist == "dup":
         return duplicates(n, dim, seed)
     raise ValueError(dist)
