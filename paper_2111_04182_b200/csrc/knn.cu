@@ -648,8 +648,17 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
     }
     // root-based search (ablation): Alg. 2 from the root with an empty list, no
     // leaf seed and no ascent; leaf-based (default): seed with the packet's leaves
-    const int32_t ps_lo = A.root_based ? 0 : __ldg(A.leaf_start + lA);
-    const int32_t ps_hi = A.root_based ? 0 : __ldg(A.leaf_start + lB + 1);
+#ifndef ZD_SEED_PAD
+#define ZD_SEED_PAD 1   // extra Morton-adjacent leaves scanned on each side of the seed
+#endif
+    int32_t sA = lA, sB = lB;
+    if (ZD_SEED_PAD > 0 && !A.root_based) {
+        const int32_t nleaves = __ldg(A.d_meta) + 1;
+        sA = max(0, lA - ZD_SEED_PAD);
+        sB = min(nleaves - 1, lB + ZD_SEED_PAD);
+    }
+    const int32_t ps_lo = A.root_based ? 0 : __ldg(A.leaf_start + sA);
+    const int32_t ps_hi = A.root_based ? 0 : __ldg(A.leaf_start + sB + 1);
     if (!A.root_based) scan_span<DIM, K>(A.recs, ps_lo, ps_hi, active, L, S, lane);
 
     if (can_defer && !A.root_based) {
