@@ -324,7 +324,7 @@ __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Qu
 #define ZD_SLACK 4          // uniform compaction when a needing lane has > CAP - SLACK entries
 #endif
 #ifndef ZD_TRANSPOSE_MAX
-#define ZD_TRANSPOSE_MAX 4   // at most this many needing lanes: lanes = candidates
+#define ZD_TRANSPOSE_MAX 6   // at most this many needing lanes: lanes = candidates
 #endif
 template <int DIM, int K>
 __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t s, int32_t e, bool need,
@@ -597,7 +597,7 @@ struct PacketArgs {
 };
 
 #ifndef ZD_INCOHERENT
-#define ZD_INCOHERENT 1024.0f   // defer a packet if its extent^2 > this * median bound
+#define ZD_INCOHERENT 4096.0f   // defer a packet if its extent^2 > this * median bound
 #endif
 
 
