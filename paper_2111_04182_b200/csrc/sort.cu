@@ -129,7 +129,15 @@ __global__ void __launch_bounds__(ST) onesweep_kernel(
         // applied in issue order, so key j's group precedes key j+1's — stable) and
         // broadcasts the old value; no __syncwarp chain between the SI keys
         const uint32_t d = (uint32_t)(key[j] >> shift) & 255u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        // lanes with the same digit: 8 ballots (one per digit bit) instead of the
+        // slow match.any
+        uint32_t peers = 0xffffffffu;
+#pragma unroll
+        for (int bit = 0; bit < 8; ++bit) {
+            const bool on = (d >> bit) & 1u;
+            const uint32_t bv = __ballot_sync(0xffffffffu, on);
+            peers &= on ? bv : ~bv;
+        }
         const int leader = __ffs(peers) - 1;
         uint32_t old = 0;
         if (lane == leader) old = atomicAdd(&u.hist[w][d], (uint32_t)__popc(peers));
