@@ -4,7 +4,7 @@
 // order"), P:416 (Thm 2.1: "a parallel radix sort can be used").
 // B200 design (not the paper's): 8 passes of 8-bit digits over 64-bit keys; one
 // up-front histogram kernel computes all 8 digit histograms while encoding (and
-// range-checking) the points; each pass is ONE kernel that ranks a 3840-key tile
+// range-checking) the points; each pass is ONE kernel that ranks a 2816-key tile
 // with warp-level match, publishes its per-digit counts, resolves its global
 // offsets by decoupled look-back over predecessor tiles (dynamic tile ids, so
 // every predecessor is resident or done), stages the tile in shared memory in
@@ -21,8 +21,14 @@ namespace zd {
 namespace {
 
 constexpr int ST = 256;              // threads per tile
-constexpr int SI = 15;               // keys per thread
-constexpr int STILE = ST * SI;       // 3840 keys per tile
+#ifndef ZD_SORT_SI
+#define ZD_SORT_SI 11
+#endif
+#ifndef ZD_SORT_MINB
+#define ZD_SORT_MINB 4
+#endif
+constexpr int SI = ZD_SORT_SI;       // keys per thread
+constexpr int STILE = ST * SI;       // 2816 keys per tile (256 threads x 11)
 constexpr int SW = ST / 32;          // warps
 constexpr int WITEMS = 32 * SI;      // contiguous keys per warp
 constexpr int NPASS = 8;
@@ -75,7 +81,7 @@ __global__ void __launch_bounds__(256) scan_hist_kernel(const uint32_t* __restri
 
 // MODE 0: first pass (encode points), 1: middle pass, 2: last pass (write records).
 template <int DIM, int MODE>
-__global__ void __launch_bounds__(ST) onesweep_kernel(
+__global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
     const int32_t* __restrict__ pts, const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ ids_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ ids_out, int4* __restrict__ recs_out,
     uint32_t n, int shift, uint32_t id_base, const uint32_t* __restrict__ digit_offs,
