@@ -146,6 +146,16 @@ class ClockSampler:
 BAD_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
 
 
+def _hbm_peak_gbs() -> float:
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return 6650.0   # B200_PROFILING.md fallback
+
+
+HBM_PEAK_GBS = _hbm_peak_gbs()
+
+
 def workload_inputs(scale_n: int | None = None):
     c = zdgen.CONFIGS[WORKLOAD]
     n = c["n"] if scale_n is None else scale_n
@@ -393,6 +403,12 @@ def run_gpu(args, D: Dist):
         "phases_ms": {"build": float(mean_ph[0]), "insert": float(mean_ph[1]), "delete": float(mean_ph[2]),
                       "knn_call": float(mean_ph[3]), "knn_kernel": knn_ms},
         "build_mpts_s": c["n"] / (mean_ph[0] / 1e3) / 1e6,
+        # build against HBM: SURVEY §8(d) algorithmic bytes (3D: encode 20 + sort 196 +
+        # records 28 + topology/boxes 30.6 = 274.6 B/point) / build time / measured copy BW
+        "build_roofline": {"bound": "hbm", "bytes_per_point": 274.6,
+                           "achieved": 274.6 * c["n"] / (mean_ph[0] / 1e3) / 1e9, "unit": "GB/s",
+                           "peak": HBM_PEAK_GBS, "frac": 274.6 * c["n"] / (mean_ph[0] / 1e3) / 1e9 / HBM_PEAK_GBS,
+                           "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
         "insert_mpts_s": c["insert_m"] / (mean_ph[1] / 1e3) / 1e6,
         "delete_mpts_s": c["delete_m"] / (mean_ph[2] / 1e3) / 1e6,
         "knn_qps": n_live / (mean_ph[3] / 1e3),
@@ -401,7 +417,7 @@ def run_gpu(args, D: Dist):
                      "traffic": traffic, "traffic_source": traffic_src,
                      "ops_per_query": ops_q, "counters_per_query": per_q,
                      "peak_note": "derived: 148 SMs x 4 SMSPs x 32 lanes x sm_max clock (B200_PROFILING.md)",
-                     "hbm_frac_compulsory": compulsory_bytes_q * n_live / (knn_ms / 1e3) / 6460.5e9},
+                     "hbm_frac_compulsory": compulsory_bytes_q * n_live / (knn_ms / 1e3) / (HBM_PEAK_GBS * 1e9)},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_tot / args.e2e_steps, "matches_device_result": same},
