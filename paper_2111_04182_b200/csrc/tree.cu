@@ -154,32 +154,75 @@ __device__ __forceinline__ void store_box(typename BoxT<DIM>::T* dst, const int3
     for (int a = 0; a < 2 * DIM; ++a) dst[a] = (typename BoxT<DIM>::T)b[a];   // exact (3D: < 2^21)
 }
 
+// One block per window of BW consecutive leaves.  An internal node whose whole leaf
+// range lies in the window gets both of its arrivals from this block, so its arrival
+// counter lives in shared memory and the release/acquire pair is block-scoped (no
+// device fence, no L1 invalidation); only window-crossing nodes use the device-scope
+// protocol.  A node's range is bounded by the nearest larger split bit on each side
+// (the canonical tree is the Cartesian tree of the split bits), found by scanning the
+// window's split bits in shared memory.
+constexpr int BW = 128;
+
 template <int DIM>
-__global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__ recs, const int32_t* __restrict__ leaf_start,
-                                                        const int32_t* __restrict__ split_bit, int32_t* meta,
-                                                        Node<DIM>* nodes, int32_t* __restrict__ leaf_parent,
-                                                        uint32_t* visit, int32_t* range, int2* __restrict__ pos_range) {
+__global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ recs, const int32_t* __restrict__ leaf_start,
+                                                       const int32_t* __restrict__ split_bit, int32_t* meta,
+                                                       Node<DIM>* nodes, int32_t* __restrict__ leaf_parent,
+                                                       uint32_t* visit, int32_t* range, int2* __restrict__ pos_range) {
+    __shared__ int32_t s_sb[BW + 1];      // split bits of nodes b0-1 .. b0+BW-1 (INT32_MAX outside [0, nb))
+    __shared__ int32_t s_ls[BW + 1];      // leaf_start[b0 .. b0+BW]
+    __shared__ uint8_t s_local[BW];       // node b0+t finishes inside this block
+    __shared__ uint32_t s_visit[BW];      // block-local arrival counters
+    __shared__ int32_t s_rng[BW][2];      // block-local nodes: children's leaf bounds (L of left, R of right)
+    __shared__ int32_t s_box[BW][2][2 * DIM];   // block-local nodes: children's boxes
     const int32_t nb = meta[0];
-    for (int32_t l = blockIdx.x * blockDim.x + threadIdx.x; l <= nb; l += gridDim.x * blockDim.x) {
-        // leaf box from its records
+    const int32_t b0 = blockIdx.x * BW;
+    if (b0 > nb) return;                  // block-uniform
+    const int t = threadIdx.x;
+    for (int i = t; i <= BW; i += BW) {
+        const int32_t q = b0 - 1 + i;
+        s_sb[i] = (q >= 0 && q < nb) ? __ldg(split_bit + q) : INT32_MAX;
+        s_ls[i] = b0 + i <= nb + 1 ? leaf_start[b0 + i] : 0;
+    }
+    __syncthreads();
+    {
+        bool loc = false;
+        if (b0 + t < nb) {   // node b0+t = s_sb[t+1]
+            const int32_t d = s_sb[t + 1];
+            bool lok = false, rok = false;
+            for (int i = t; i >= 0; --i) if (s_sb[i] > d) { lok = true; break; }
+            for (int i = t + 2; i <= BW; ++i) if (s_sb[i] > d) { rok = true; break; }
+            loc = lok && rok;
+        }
+        s_local[t] = loc;
+        s_visit[t] = 0u;
+    }
+    __syncthreads();
+    const int32_t l = b0 + t;
+    if (l > nb) return;
+    // split bit of node q / start of leaf q, from shared memory inside the window
+    auto sbit = [&](int32_t q) { return (q >= b0 - 1 && q < b0 + BW) ? s_sb[q - b0 + 1] : __ldg(split_bit + q); };
+    auto lstart = [&](int32_t q) { return (q >= b0 && q <= b0 + BW) ? s_ls[q - b0] : __ldg(leaf_start + q); };
+    {
+        // leaf box from its records (independent loads, unrolled)
         int32_t bb[2 * DIM];
 #pragma unroll
         for (int a = 0; a < DIM; ++a) { bb[a] = INT32_MAX; bb[DIM + a] = INT32_MIN; }
-        const int32_t s = leaf_start[l], e = leaf_start[l + 1];
+        const int32_t s = s_ls[t], e = lstart(l + 1);
+#pragma unroll 4
         for (int32_t j = s; j < e; ++j) {
             const int4 r = __ldg(recs + j);
             const int c[3] = {r.x, r.y, r.z};
 #pragma unroll
             for (int a = 0; a < DIM; ++a) { bb[a] = min(bb[a], c[a]); bb[DIM + a] = max(bb[DIM + a], c[a]); }
         }
-        if (nb == 0) { leaf_parent[0] = -1; continue; }
+        if (nb == 0) { leaf_parent[0] = -1; return; }
         int32_t L = l, R = l, ref = -1;   // ref: internal node index, -1 while at the leaf
         while (true) {
             bool as_right;
             int32_t par;
             if (L == 0) { par = R; as_right = false; }
             else if (R == nb) { par = L - 1; as_right = true; }
-            else if (__ldg(split_bit + L - 1) < __ldg(split_bit + R)) { par = L - 1; as_right = true; }
+            else if (sbit(L - 1) < sbit(R)) { par = L - 1; as_right = true; }
             else { par = R; as_right = false; }
             ZD_DCHECK(par >= 0 && par < nb && L >= 0 && R <= nb);
             Node<DIM>* P = nodes + par;
@@ -188,20 +231,38 @@ __global__ void __launch_bounds__(128) bottom_up_kernel(const int4* __restrict__
             if (as_right) { store_box<DIM>(P->rbox, bb); P->right = cref; range[2 * par + 1] = R; }
             else { store_box<DIM>(P->lbox, bb); P->left = cref; range[2 * par] = L; }
             if (ref < 0) leaf_parent[l] = par; else nodes[ref].parent = par;
-            // release: our box/ref/range writes are visible before the count; acquire:
-            // the second arriver sees its sibling's (one MEMBAR + one L1 invalidate,
-            // instead of two sequentially consistent fences)
-            const uint32_t arrived =
-                cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(visit[par]).fetch_add(1u, cuda::memory_order_acq_rel);
-            if (arrived == 0) break;   // first child: the sibling finishes the parent
-            const typename BoxT<DIM>::T* sb = as_right ? P->lbox : P->rbox;
+            const bool loc = par >= b0 && par < b0 + BW && s_local[par - b0];
+            if (loc) {
+                // both children of par finish in this block: exchange through shared
+                // memory with a block-scoped release/acquire
+                const int pi = par - b0, side = as_right ? 1 : 0;
 #pragma unroll
-            for (int a = 0; a < DIM; ++a) {
-                bb[a] = min(bb[a], (int32_t)__ldcg(sb + a));
-                bb[DIM + a] = max(bb[DIM + a], (int32_t)__ldcg(sb + DIM + a));
+                for (int a = 0; a < 2 * DIM; ++a) s_box[pi][side][a] = bb[a];
+                s_rng[pi][side] = as_right ? R : L;
+                __threadfence_block();
+                if (atomicAdd(&s_visit[pi], 1u) == 0) break;
+                __threadfence_block();
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    bb[a] = min(bb[a], s_box[pi][side ^ 1][a]);
+                    bb[DIM + a] = max(bb[DIM + a], s_box[pi][side ^ 1][DIM + a]);
+                }
+                if (as_right) L = s_rng[pi][0]; else R = s_rng[pi][1];
+            } else {
+                // release: our writes are visible before the count; acquire: the second
+                // arriver sees its sibling's
+                const uint32_t arrived =
+                    cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(visit[par]).fetch_add(1u, cuda::memory_order_acq_rel);
+                if (arrived == 0) break;   // first child: the sibling finishes the parent
+                const typename BoxT<DIM>::T* sb = as_right ? P->lbox : P->rbox;
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    bb[a] = min(bb[a], (int32_t)__ldcg(sb + a));
+                    bb[DIM + a] = max(bb[DIM + a], (int32_t)__ldcg(sb + DIM + a));
+                }
+                if (as_right) L = __ldcg(range + 2 * par); else R = __ldcg(range + 2 * par + 1);
             }
-            if (as_right) L = __ldcg(range + 2 * par); else R = __ldcg(range + 2 * par + 1);
-            pos_range[par] = make_int2(__ldg(leaf_start + L), __ldg(leaf_start + R + 1));
+            pos_range[par] = make_int2(lstart(L), lstart(R + 1));
             ref = par;
             if (L == 0 && R == nb) { P->parent = -1; meta[1] = par; break; }
         }
@@ -259,15 +320,15 @@ void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // about one thread per leaf (leaves <= n / 4 unless leaf_max is tiny: grid-stride)
+    // one block per BW-leaf window; leaves <= max(n, 1) (empty windows exit at once)
     (void)sms;
-    int grid = (int)std::max<int64_t>(1, (n / 4 + 127) / 128);
+    int grid = (int)std::max<int64_t>(1, (std::max<int64_t>(n, 1) + BW - 1) / BW);
     count_launch(1);
     if (dim == 2)
-        bottom_up_kernel<2><<<grid, 128, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<2>*)t.nodes,
+        bottom_up_kernel<2><<<grid, BW, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<2>*)t.nodes,
                                                   t.leaf_parent, t.visit, t.range, t.pos_range);
     else
-        bottom_up_kernel<3><<<grid, 128, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<3>*)t.nodes,
+        bottom_up_kernel<3><<<grid, BW, 0, st>>>(recs, t.leaf_start, t.split_bit, t.d_meta, (Node<3>*)t.nodes,
                                                   t.leaf_parent, t.visit, t.range, t.pos_range);
 }
 
