@@ -180,6 +180,9 @@ template <int DIM>
 __device__ __forceinline__ Ref right_child(const Node<DIM>& nd, int32_t e) { return child_ref(nd.right, nd.mid, e); }
 
 
+#ifndef ZD_PREFETCH_CHILDREN
+#define ZD_PREFETCH_CHILDREN 0
+#endif
 #ifndef ZD_F32FILTER
 #define ZD_F32FILTER 1   // 3D: candidate tests in fp32 (exact coordinates), confirmed in int64
 #endif
@@ -509,6 +512,11 @@ __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const 
             ZD_DCHECK(cur.ref < S.dbg_nint && cur.s < cur.e && cur.e <= S.dbg_npts);
 #endif
             const Node<DIM> nd = load_node<DIM>(nodes + cur.ref);
+#if ZD_PREFETCH_CHILDREN
+            // warm L1 with both internal children while the boxes are tested
+            if (lane == 0 && nd.left >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(nodes + nd.left));
+            if (lane == 1 && nd.right >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(nodes + nd.right));
+#endif
             const typename BoxD<DIM>::T dl = box_dist<DIM, K>(L, nd.lbox), dr = box_dist<DIM, K>(L, nd.rbox);
             const bool ln = within<DIM, K>(L, dl), rn = within<DIM, K>(L, dr);
             const bool nl = __any_sync(0xffffffffu, ln), nr = __any_sync(0xffffffffu, rn);
