@@ -152,6 +152,9 @@ constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
 #endif
 constexpr int kStk = ZD_STK;             // per-warp stack entries (>= tree height; 64 = key bits + 1)
 
+#ifndef ZD_MINB16
+#define ZD_MINB16 5       // min resident blocks per SM for 10 < K <= 16
+#endif
 #ifndef ZD_CAP_MIN
 #define ZD_CAP_MIN 22
 #endif
@@ -811,7 +814,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
 }
 
 template <int DIM, int K, bool EXT>
-__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? ZD_MINB : 2)) knn_packet_kernel(PacketArgs A) {
+__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? ZD_MINB : (K <= 16 ? ZD_MINB16 : 2))) knn_packet_kernel(PacketArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSh<K>* sh = reinterpret_cast<WarpSh<K>*>(smem_raw);   // Pw<K>::v warps
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
