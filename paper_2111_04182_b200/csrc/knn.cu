@@ -189,12 +189,24 @@ __device__ __forceinline__ Ref right_child(const Node<DIM>& nd, int32_t e) { ret
 #ifndef ZD_F32FILTER
 #define ZD_F32FILTER 1   // 3D: candidate tests in fp32 (exact coordinates), confirmed in int64
 #endif
+#ifndef ZD_PREFILTER
+#define ZD_PREFILTER 1   // drop staged candidates outside the packet box dilated by the span's max bound
+#endif
+#ifndef ZD_PREGROUPS
+#define ZD_PREGROUPS 1   // prefilter boxes per packet (groups of 32 / G Morton-consecutive lanes)
+#endif
+constexpr int kPG = ZD_PREGROUPS, kPGW = 32 / ZD_PREGROUPS;
+#ifndef ZD_PREFILTER2D
+#define ZD_PREFILTER2D 0 // the same in 2D (exact int64; measured slightly slower on C2 / 2D Kuzmin)
+#endif
 template <int K>
 struct WarpSh {
     int4 c[32];                          // staged candidates (x, y, z|0, id)
 #if ZD_F32FILTER
     float4 f[32];                        // 3D: the same in fp32 (exact below 2^24)
 #endif
+    int32_t p[32];                       // their sorted positions
+    float4 pb[2 * kPG];                  // query box of each lane group (lo, hi; 2D: int bits)
     int32_t bp[Cap<K>::v][32];           // per-lane buffered positions; column = lane
     float bf[Cap<K>::v][32];             //   ... and their d2 rounded up to fp32
     int4 stk[kStk];                      // (ref, s, e, parent | side << 31): box reloaded on pop
@@ -339,18 +351,79 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
     if (M == 0) return;
     const int w = __popc(M);
     ZD_STAT(ZS_SPANS, 1);
+#if ZD_PREFILTER
+    // Packet prefilter (uniform mode): a candidate c that some needing lane i accepts
+    // is within that lane's bound, bound_i <= bmax (max over the needing lanes), and
+    // the distance from c to the packet's query box is at most d2(q_i, c) (per-axis
+    // gaps <= |q_i - c|): exact in 2D (int64); in 3D the fp32 box distance uses the
+    // same evaluation order on exact per-axis gaps and every rounding is monotone, so
+    // it is <= the lane's fp32 d2 <= wb_i.  So dropping c when the box distance exceeds
+    // bmax loses nothing; bounds only shrink, so bmax taken here stays valid.
+    const bool uni = (DIM == 3 || ZD_PREFILTER2D) && w > ZD_TRANSPOSE_MAX;
+    typename BoxD<DIM>::T bmax;
+    if constexpr (DIM == 3) bmax = need ? L.wb : -1.0f;
+    else bmax = need ? L.U : (int64_t)-1;
+    typename BoxD<DIM>::T gm[kPG];   // per lane group (-1: no needing lane in it)
+    bool pre = false;
+    if (uni) {
+#pragma unroll
+        for (int o = kPGW >> 1; o > 0; o >>= 1) {
+            const typename BoxD<DIM>::T ob = __shfl_xor_sync(0xffffffffu, bmax, o);
+            bmax = ob > bmax ? ob : bmax;
+        }
+        pre = true;
+#pragma unroll
+        for (int g = 0; g < kPG; ++g) {
+            gm[g] = __shfl_sync(0xffffffffu, bmax, g * kPGW);
+            if constexpr (DIM == 3) pre = pre && gm[g] != INFINITY;
+            else pre = pre && gm[g] != INT64_MAX;
+        }
+    }
+#endif
     for (int32_t b = s; b < e; b += 32) {
-        const int n32 = min(32, e - b);
+        const int n32r = min(32, e - b);
         __syncwarp();
-        if (lane < n32) {
+        int4 r = make_int4(0, 0, 0, 0);
+        float4 fc = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool keep = lane < n32r;
+        if (keep) {
 #ifdef ZD_DEBUG
             ZD_DCHECK(b >= 0 && b + lane < S.dbg_npts);
 #endif
-            const int4 r = __ldg(recs + b + lane);
-            S.c[lane] = r;
+            r = __ldg(recs + b + lane);
 #if ZD_F32FILTER
             if (DIM == 3)
-                S.f[lane] = make_float4(__int2float_rn(r.x), __int2float_rn(r.y), __int2float_rn(r.z), __int_as_float(r.w));
+                fc = make_float4(__int2float_rn(r.x), __int2float_rn(r.y), __int2float_rn(r.z), __int_as_float(r.w));
+#endif
+#if ZD_PREFILTER
+            if (pre) {
+                keep = false;
+#pragma unroll
+                for (int g = 0; g < kPG; ++g) {
+                    const float4 lo = S.pb[2 * g], hi = S.pb[2 * g + 1];
+                    if constexpr (DIM == 3) {
+                        const float tx = fmaxf(lo.x - fc.x, 0.f) + fmaxf(fc.x - hi.x, 0.f);
+                        const float ty = fmaxf(lo.y - fc.y, 0.f) + fmaxf(fc.y - hi.y, 0.f);
+                        const float tz = fmaxf(lo.z - fc.z, 0.f) + fmaxf(fc.z - hi.z, 0.f);
+                        keep = keep || fmaf(tz, tz, fmaf(ty, ty, tx * tx)) <= gm[g];
+                    } else {
+                        const int tx = max(__float_as_int(lo.x) - r.x, 0) + max(r.x - __float_as_int(hi.x), 0);
+                        const int ty = max(__float_as_int(lo.y) - r.y, 0) + max(r.y - __float_as_int(hi.y), 0);
+                        keep = keep || (int64_t)tx * tx + (int64_t)ty * ty <= gm[g];
+                    }
+                }
+            }
+#endif
+        }
+        const uint32_t km = __ballot_sync(0xffffffffu, keep);
+        const int n32 = __popc(km);
+        if (n32 == 0) continue;
+        if (keep) {
+            const int slot = __popc(km & ((1u << lane) - 1u));
+            S.c[slot] = r;
+            S.p[slot] = b + lane;
+#if ZD_F32FILTER
+            if (DIM == 3) S.f[slot] = fc;
 #endif
         }
         __syncwarp();
@@ -470,7 +543,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                     }
                 }
                 ZD_DCHECK(L.cnt < Cap<K>::v);
-                S.bp[L.cnt][lane] = b + j;
+                S.bp[L.cnt][lane] = S.p[j];
                 S.bf[L.cnt][lane] = xf;
                 ++L.cnt;
             }
@@ -638,6 +711,40 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
     L.qf[0] = __int2float_rn(r.x); L.qf[1] = __int2float_rn(r.y); L.qf[2] = __int2float_rn(r.z);
     L.wb = active ? INFINITY : -1.0f;
     L.cnt = 0;
+#if ZD_PREFILTER
+    if (DIM == 3 || ZD_PREFILTER2D) {
+        // the packet's query box for the prefilter (idle lanes hold a copy of query p0);
+        // 3D in fp32 (exact), 2D as int32 bit patterns
+        float lo[DIM], hi[DIM];
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            if constexpr (DIM == 3) {
+                lo[a] = L.qf[a];
+                hi[a] = L.qf[a];
+            }
+            int il = L.q.c[a], ih = L.q.c[a];
+#pragma unroll
+            for (int o = kPGW >> 1; o > 0; o >>= 1) {
+                if constexpr (DIM == 3) {
+                    lo[a] = fminf(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+                    hi[a] = fmaxf(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+                } else {
+                    il = min(il, __shfl_xor_sync(0xffffffffu, il, o));
+                    ih = max(ih, __shfl_xor_sync(0xffffffffu, ih, o));
+                }
+            }
+            if constexpr (DIM == 2) {
+                lo[a] = __int_as_float(il);
+                hi[a] = __int_as_float(ih);
+            }
+        }
+        if ((lane & (kPGW - 1)) == 0) {
+            S.pb[2 * (lane / kPGW)] = make_float4(lo[0], lo[1], DIM == 3 ? lo[DIM - 1] : 0.f, 0.f);
+            S.pb[2 * (lane / kPGW) + 1] = make_float4(hi[0], hi[1], DIM == 3 ? hi[DIM - 1] : 0.f, 0.f);
+        }
+        __syncwarp();
+    }
+#endif
 
     int32_t lA, lB;
     if (!EXT) {
