@@ -167,20 +167,25 @@ struct Cap {   // buffered candidates per lane (overflow compacts per lane: any 
 // points [~ref, end).
 // A subtree in traversal form with its sorted point range [s, e): ref >= 0 an
 // internal node; ref < 0 a contiguous span scanned directly — a leaf, or (query-side
-// coarsening) a subtree of at most ZD_COARSE points, whose points are contiguous too.
+// coarsening) a subtree of at most Coarse<DIM> points, whose points are contiguous too.
 #ifndef ZD_COARSE
-#define ZD_COARSE 32
+#define ZD_COARSE 32    // 2D
+#endif
+#ifndef ZD_COARSE3
+#define ZD_COARSE3 64   // 3D (with the fp32 prefilter wide spans are cheap)
 #endif
 struct Ref {
     int32_t ref, s, e;
 };
+template <int DIM>
 __device__ __forceinline__ Ref child_ref(int32_t c, int32_t s, int32_t e) {
-    return (c < 0 || e - s <= ZD_COARSE) ? Ref{~s, s, e} : Ref{c, s, e};
+    constexpr int32_t coarse = DIM == 3 ? ZD_COARSE3 : ZD_COARSE;
+    return (c < 0 || e - s <= coarse) ? Ref{~s, s, e} : Ref{c, s, e};
 }
 template <int DIM>
-__device__ __forceinline__ Ref left_child(const Node<DIM>& nd, int32_t s) { return child_ref(nd.left, s, nd.mid); }
+__device__ __forceinline__ Ref left_child(const Node<DIM>& nd, int32_t s) { return child_ref<DIM>(nd.left, s, nd.mid); }
 template <int DIM>
-__device__ __forceinline__ Ref right_child(const Node<DIM>& nd, int32_t e) { return child_ref(nd.right, nd.mid, e); }
+__device__ __forceinline__ Ref right_child(const Node<DIM>& nd, int32_t e) { return child_ref<DIM>(nd.right, nd.mid, e); }
 
 
 #ifndef ZD_PREFETCH_CHILDREN
@@ -342,8 +347,15 @@ __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Qu
 #define ZD_SLACK 4          // uniform compaction when a needing lane has > CAP - SLACK entries
 #endif
 #ifndef ZD_TRANSPOSE_MAX
-#define ZD_TRANSPOSE_MAX 6   // at most this many needing lanes: lanes = candidates
+#define ZD_TRANSPOSE_MAX 6   // 2D: at most this many needing lanes: lanes = candidates
 #endif
+#ifndef ZD_TRANSPOSE_MAX3
+#define ZD_TRANSPOSE_MAX3 2  // 3D
+#endif
+template <int DIM>
+struct TMax {
+    static constexpr int v = DIM == 3 ? ZD_TRANSPOSE_MAX3 : ZD_TRANSPOSE_MAX;
+};
 template <int DIM, int K>
 __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t s, int32_t e, bool need,
                                           Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
@@ -359,7 +371,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
     // same evaluation order on exact per-axis gaps and every rounding is monotone, so
     // it is <= the lane's fp32 d2 <= wb_i.  So dropping c when the box distance exceeds
     // bmax loses nothing; bounds only shrink, so bmax taken here stays valid.
-    const bool uni = (DIM == 3 || ZD_PREFILTER2D) && w > ZD_TRANSPOSE_MAX;
+    const bool uni = (DIM == 3 || ZD_PREFILTER2D) && w > TMax<DIM>::v;
     typename BoxD<DIM>::T bmax;
     if constexpr (DIM == 3) bmax = need ? L.wb : -1.0f;
     else bmax = need ? L.U : (int64_t)-1;
@@ -436,7 +448,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 compact<DIM, K>(L, S, lane);
             }
             uint32_t hit = 0;
-            if (w > ZD_TRANSPOSE_MAX) {
+            if (w > TMax<DIM>::v) {
                 // every lane tests every candidate against its own bound
 #if ZD_F32FILTER
                 if (DIM == 3) {
@@ -830,7 +842,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
     bool sub_need = active;
     if (A.root_based) {
         const int32_t root = __ldg(A.d_meta + 1);   // internal index, or ~0 for a single leaf
-        sub = root >= 0 ? child_ref(root, 0, A.n_pts) : Ref{~0, 0, A.n_pts};
+        sub = root >= 0 ? child_ref<DIM>(root, 0, A.n_pts) : Ref{~0, 0, A.n_pts};
         P = -1;
     } else if (lA == lB) {
         P = __ldg(A.leaf_parent + lA);
@@ -852,7 +864,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         C = x;
         P = __ldg(&nodes[x].parent);
         const int2 xr = __ldg(A.pos_range + x);
-        sub = child_ref(x, xr.x, xr.y);
+        sub = child_ref<DIM>(x, xr.x, xr.y);
     }
     while (true) {
         if (sub.ref != kNoSub) joint_down<DIM, K>(A.recs, nodes, sub, sub_need, ps_lo, ps_hi, L, S, lane);
