@@ -71,7 +71,7 @@ enum {
     ZD_ECUDA = -4     /* any other CUDA runtime error */
 };
 
-#define ZD_K_MAX 32        /* largest k served by zd_knn */
+#define ZD_K_MAX 128       /* largest k served by zd_knn (k > 32: warp-per-query path) */
 #define ZD_LEAF_MAX_MAX 32 /* largest leaf size accepted by zd_build_ex */
 
 typedef struct zd_opts {
@@ -104,8 +104,11 @@ ZD_API int zd_knn(zd_tree *h, const int32_t *queries, int64_t m, int k,
  * starts at its own leaf and ascends, Alg. 3); ZD_KNN_ROOT_BASED = the
  * root-based variant (Alg. 2 from the root with an empty neighbour list), kept
  * as an ablation — the answer is identical, the work differs (the paper's Fig. 2).
- * Unknown flags -> ZD_EINVAL. */
+ * ZD_KNN_WARP = run the large-k kernel (one warp per query, warp-shared top-k buffer
+ * with radix selection; P:543's large-k container) for any k; it
+ * always serves k > 32.  Flags combine.  Unknown flags -> ZD_EINVAL. */
 #define ZD_KNN_ROOT_BASED 1
+#define ZD_KNN_WARP 2
 ZD_API int zd_knn_ex(zd_tree *h, const int32_t *queries, int64_t m, int k,
               int32_t *out_idx, int64_t *out_dist2, int flags);
 

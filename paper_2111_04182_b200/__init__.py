@@ -22,8 +22,9 @@ from pathlib import Path
 from ._build import LIB_PATH, STATS_LIB_PATH, build_lib
 
 ZD_OK, ZD_EINVAL, ZD_ERANGE, ZD_ENOMEM, ZD_ECUDA = 0, -1, -2, -3, -4
-ZD_K_MAX = 32
+ZD_K_MAX = 128
 ZD_KNN_ROOT_BASED = 1
+ZD_KNN_WARP = 2
 ZD_LEAF_MAX_MAX = 32
 PHASES = ("sort", "topology", "bbox", "merge_compact", "knn", "validate")
 
@@ -168,11 +169,14 @@ class ZdTree:
         return self._h
 
     # -- queries
-    def zd_knn(self, k: int, queries=None, out_idx=None, out_dist2=None, device=None, root_based: bool = False):
+    def zd_knn(self, k: int, queries=None, out_idx=None, out_dist2=None, device=None, root_based: bool = False,
+               warp: bool = False):
         """Exact k-NN.  queries=None: all live points (rows by ascending live id).
         Returns (out_idx int32 [m,k], out_dist2 int64 [m,k]); allocated on `device`
         (default: cuda) when not given.  root_based=True: the root-based search
-        variant (zd_knn_ex, ZD_KNN_ROOT_BASED), same answer."""
+        variant (zd_knn_ex, ZD_KNN_ROOT_BASED); warp=True: the large-k
+        warp-per-query kernel for any k (ZD_KNN_WARP; always used for k > 32).  Same
+        answer either way."""
         import torch
         q = None if queries is None else _as_i32(queries)
         m = self.zd_size() if q is None else int(q.shape[0])
@@ -180,8 +184,9 @@ class ZdTree:
             dev = device or "cuda"
             out_idx = torch.empty((m, k), dtype=torch.int32, device=dev)
             out_dist2 = torch.empty((m, k), dtype=torch.int64, device=dev)
-        if root_based:
-            _check(load().zd_knn_ex(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2), ZD_KNN_ROOT_BASED))
+        flags = (ZD_KNN_ROOT_BASED if root_based else 0) | (ZD_KNN_WARP if warp else 0)
+        if flags:
+            _check(load().zd_knn_ex(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2), flags))
         else:
             _check(load().zd_knn(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2)))
         return out_idx, out_dist2
@@ -265,5 +270,5 @@ def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None,
     return ZdTree(h, dim)
 
 
-__all__ = ["zd_build", "zd_kernel_launches", "zd_knn_stats", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "PHASES",
+__all__ = ["zd_build", "zd_kernel_launches", "zd_knn_stats", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "ZD_KNN_WARP", "PHASES",
            "ZD_OK", "ZD_EINVAL", "ZD_ERANGE", "ZD_ENOMEM", "ZD_ECUDA"]

@@ -428,7 +428,7 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
 
 int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_idx, int64_t* out_dist2, int flags) {
     clear_err();
-    if (flags & ~ZD_KNN_ROOT_BASED) return fail(ZD_EINVAL, "zd_knn_ex: unknown flags");
+    if (flags & ~(ZD_KNN_ROOT_BASED | ZD_KNN_WARP)) return fail(ZD_EINVAL, "zd_knn_ex: unknown flags");
     if (!h) return fail(ZD_EINVAL, "NULL handle");
     if (k < 1 || k > ZD_K_MAX) return fail(ZD_EINVAL, "zd_knn: k must be in [1, ZD_K_MAX]");
     if (m < 0 || m >= ((int64_t)1 << 31) - 1) return fail(ZD_EINVAL, "zd_knn: bad m");
@@ -456,6 +456,7 @@ int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out
     a.hard_list = hard + 2;
     a.hard_cap = kHardCap;
     a.root_based = (flags & ZD_KNN_ROOT_BASED) ? 1 : 0;
+    a.warp = (flags & ZD_KNN_WARP) ? 1 : 0;
     // ZD_KNN_DEFER (testing): "none" = no second pass, "all" = every packet deferred
     // (up to the list capacity); default: incoherent packets only
     if (const char* dm = std::getenv("ZD_KNN_DEFER")) {

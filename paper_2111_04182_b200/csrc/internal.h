@@ -71,8 +71,11 @@ struct KnnArgs {
     int hard_cap;
     int defer_all;               // testing: every packet goes to the second pass
     int root_based;              // ablation: root-based search
+    int warp;                    // the warp-per-query kernel (knn_warp.cu) for any k
 };
-int knn_kmax();
+constexpr int kPacketKMax = 32;   // largest k of the packet kernel; above: knn_warp
+// Large-k path (knn_warp.cu): one warp per query over Morton-ordered queries.
+void knn_warp(const KnnArgs& a, const int4* qrecs, const int32_t* qleaf, int64_t nq, bool ext, cudaStream_t st);
 // Work counters of the packet k-NN kernel (only in a -DZD_KNN_STATS build).
 enum { ZS_PACKETS = 0, ZS_QUERIES, ZS_NODES, ZS_POPS, ZS_ASCENTS, ZS_SPANS, ZS_PASSES, ZS_CAND, ZS_HITS,
        ZS_ROUNDS, ZS_COMPACT, ZS_SURV, ZS_SURV_MAX, ZS_CYCLES, ZS_MAXPKT, ZS_DEFERRED, ZS_HIST0, ZD_NSTATS = ZS_HIST0 + 32 };

@@ -1029,8 +1029,6 @@ void dispatch(const PacketArgs& A, cudaStream_t st) {
 
 }  // namespace
 
-int knn_kmax() { return 32; }
-
 int knn_stats(unsigned long long* out, int n, int reset) {
 #ifdef ZD_KNN_STATS
     if (n > ZD_NSTATS) n = ZD_NSTATS;
@@ -1051,6 +1049,7 @@ void knn_all(const KnnArgs& a, cudaStream_t st) {
     A.qrecs = a.recs;
     A.qleaf = a.pt_leaf;
     A.nq = (int32_t)a.n;
+    if (a.warp || a.k > kPacketKMax) { knn_warp(a, a.recs, a.pt_leaf, a.n, false, st); return; }
     if (a.dim == 2) dispatch<2, false>(A, st); else dispatch<3, false>(A, st);
 }
 
@@ -1067,6 +1066,7 @@ void knn_queries(const KnnArgs& a, const uint64_t* qkeys, const int4* qrecs, int
     A.qrecs = qrecs;
     A.qleaf = qleaf;
     A.nq = (int32_t)m;
+    if (a.warp || a.k > kPacketKMax) { knn_warp(a, qrecs, qleaf, m, true, st); return; }
     if (a.dim == 2) dispatch<2, true>(A, st); else dispatch<3, true>(A, st);
 }
 

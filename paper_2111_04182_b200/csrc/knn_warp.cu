@@ -1,0 +1,395 @@
+// knn_warp.cu — large-k exact k-NN (k up to ZD_K_MAX): one warp per query.
+//
+// PAPER.md: Alg. 3 searchUp calling Alg. 2 searchDown,
+// leaf-based or root-based; the k-best container for large k is a
+// priority queue in the paper ("vector for small k, heap for large k"); here
+// it is a warp-cooperative buffer with radix selection.
+//
+// The packet kernel (knn.cu) keeps a k-long list per lane in registers, which stops
+// paying beyond k = 32 (register pressure).  Here one warp owns ONE query
+// and its traversal is warp-uniform (every lane computes the same node tests, so
+// nothing diverges); the 32 lanes share the leaf scans (lane = candidate) and the
+// k-best bookkeeping:
+//   buf    (exact d2, sorted position) of every candidate with d2 <= T when seen,
+//          in shared memory, appended by ballot + prefix rank;
+//   T      a bound on the exact k-th smallest d2 seen so far (INT64_MAX until k
+//          candidates are buffered); T never grows, and pruning (reading 8), the stop
+//          test (reading 9) and buffering by "d2 <= T" lose nothing;
+//   select when the buffer would overflow: radix-select (4 x 8 bits) the k-th smallest
+//          key ru(d2) (fp32 rounded up, monotone in d2), T = that key as an integer
+//          (>= the exact k-th smallest d2), keep the entries with d2 <= T.
+// At the end the survivors are ranked exactly by (d2, id) (reading 14) and the first
+// k written; short rows are padded with (-1, INT64_MAX) (reading 15).
+#include <climits>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace zd {
+namespace {
+
+constexpr int KW_CAP = 2 * 128 + 64;   // buffered candidates per query (>= ZD_K_MAX + 32)
+constexpr int KW_WARPS = 4;            // warps (queries) per block
+constexpr int KW_STK = kMaxDepth;      // DFS stack: at most one far child per tree level
+#ifndef ZD_KW_COARSE
+#define ZD_KW_COARSE 32                // subtrees of <= this many points are scanned as one span
+#endif
+#ifndef ZD_KW_MINB
+#define ZD_KW_MINB 8
+#endif
+
+struct KwSh {
+    int64_t d2[KW_CAP];
+    int32_t pos[KW_CAP];   // sorted positions; replaced by ids for the final ranking
+    uint32_t hist[256];
+    int4 stk[KW_STK];      // (ref, s, e, box d2 rounded down, fp32 bits)
+};
+
+struct KwArgs {
+    const int4* recs;
+    const int32_t* leaf_start;
+    const int32_t* leaf_parent;
+    const void* nodes;
+    const int2* pos_range;
+    const int32_t* d_meta;     // [0] internal node count, [1] root ref
+    const int4* qrecs;         // queries in Morton order (x, y, z|0, id or query index)
+    const int32_t* qleaf;      // leaf of each query
+    int32_t nq, n_pts, k;
+    const int32_t* row_of_id;
+    int32_t* out_idx;
+    int64_t* out_d2;
+    int ext, root_based;
+};
+
+struct Sub {
+    int32_t ref, s, e;   // ref >= 0 internal node; ref < 0 a span [s, e) scanned directly
+};
+__device__ __forceinline__ Sub sub_ref(int32_t c, int32_t s, int32_t e) {
+    return (c < 0 || e - s <= ZD_KW_COARSE) ? Sub{~s, s, e} : Sub{c, s, e};
+}
+
+template <int DIM>
+struct KwQuery {
+    int c[3];
+    int32_t id;   // excluded id (-1: none)
+};
+
+template <int DIM>
+__device__ __forceinline__ int64_t kw_d2(const KwQuery<DIM>& q, const int4& r) {
+    const int dx = q.c[0] - r.x, dy = q.c[1] - r.y;
+    int64_t s = (int64_t)dx * dx + (int64_t)dy * dy;
+    if (DIM == 3) {
+        const int dz = q.c[2] - r.z;
+        s += (int64_t)dz * dz;
+    }
+    return s;
+}
+
+// exact squared distance from q to a box (lo[DIM], hi[DIM]) stored as int32 (2D) or
+// exact-integer fp32 (3D); 0 inside (withinBox)
+template <int DIM>
+__device__ __forceinline__ int64_t kw_boxd2(const KwQuery<DIM>& q, const typename BoxT<DIM>::T* b) {
+    int64_t s = 0;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) {
+        const int lo = (int)b[a], hi = (int)b[DIM + a];
+        const int t = max(lo - q.c[a], 0) + max(q.c[a] - hi, 0);
+        s += (int64_t)t * t;
+    }
+    return s;
+}
+
+// Alg. 3 stop test on C's box (reading 9): q inside with margin m on every axis and
+// (m+1)^2 > T
+template <int DIM>
+__device__ __forceinline__ bool kw_stop(const KwQuery<DIM>& q, const typename BoxT<DIM>::T* b, int64_t T) {
+    int m = INT_MAX;
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) m = min(m, min(q.c[a] - (int)b[a], (int)b[DIM + a] - q.c[a]));
+    if (m < 0) return false;
+    const int64_t mm = (int64_t)m + 1;
+    return mm * mm > T;
+}
+
+__device__ __forceinline__ uint32_t kw_key(int64_t d2) { return __float_as_uint(__ll2float_ru(d2)); }
+
+struct KwState {
+    int64_t T;
+    int cnt;
+    int lim;   // re-select once cnt reaches this (first at k: the first finite bound)
+};
+
+// keep the buffered entries with d2 <= T (stable, in place: write index <= read index)
+__device__ __forceinline__ void kw_compact(KwSh& S, KwState& st, int lane) {
+    int w = 0;
+    for (int base = 0; base < st.cnt; base += 32) {
+        const int e = base + lane;
+        const bool v = e < st.cnt;
+        const int64_t d = v ? S.d2[e] : 0;
+        const int32_t p = v ? S.pos[e] : 0;
+        const bool keep = v && d <= st.T;
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        if (keep) {
+            const int slot = w + __popc(m & ((1u << lane) - 1u));
+            S.d2[slot] = d;
+            S.pos[slot] = p;
+        }
+        w += __popc(m);
+        __syncwarp();
+    }
+    st.cnt = w;
+}
+
+// T = the k-th smallest ru(d2) among the buffer (as an integer, >= the exact k-th
+// smallest d2); requires cnt >= k.  Radix selection over the fp32 key bits (non-
+// negative floats order like their bit patterns), 8 bits per pass.
+__device__ __forceinline__ void kw_select(KwSh& S, KwState& st, int k, int lane) {
+    uint32_t prefix = 0, mask = 0;
+    int kk = k;   // 1-based rank still to find among the entries matching the prefix
+#pragma unroll 1
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int i = lane; i < 256; i += 32) S.hist[i] = 0;
+        __syncwarp();
+        for (int e = lane; e < st.cnt; e += 32) {
+            const uint32_t key = kw_key(S.d2[e]);
+            if ((key & mask) == prefix) atomicAdd(&S.hist[(key >> shift) & 255u], 1u);
+        }
+        __syncwarp();
+        uint32_t h[8];
+        uint32_t loc = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            h[j] = S.hist[lane * 8 + j];
+            loc += h[j];
+        }
+        uint32_t incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t excl = incl - loc;
+        const bool mine = excl < (uint32_t)kk && (uint32_t)kk <= incl;
+        int bin = 0;
+        uint32_t below = excl;
+        if (mine) {
+            uint32_t run = excl;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (run + h[j] >= (uint32_t)kk) { bin = lane * 8 + j; below = run; break; }
+                run += h[j];
+            }
+        }
+        const int src = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        bin = __shfl_sync(0xffffffffu, bin, src);
+        below = __shfl_sync(0xffffffffu, below, src);
+        prefix |= (uint32_t)bin << shift;
+        mask |= 255u << shift;
+        kk -= (int)below;
+        __syncwarp();
+    }
+    // an fp32 value >= 2^24 is an integer, and below 2^24 ru(d2) == d2: exact conversion
+    const int64_t T = (int64_t)__uint_as_float(prefix);
+    if (T < st.T) st.T = T;
+}
+
+// Massive ties (rare): keep exactly the k best buffered entries by (d2, id).
+__device__ __noinline__ void kw_keep_exact(const int4* __restrict__ recs, KwSh& S, KwState& st, int k, int lane) {
+    const int c = st.cnt;
+    for (int base = 0; base < c; base += 32) {
+        const int e = base + lane;
+        int rank = INT_MAX;
+        if (e < c) {
+            const int64_t de = S.d2[e];
+            const int32_t ie = __ldg(recs + S.pos[e]).w;
+            rank = 0;
+            for (int f = 0; f < c; ++f) {
+                const int64_t df = S.d2[f];
+                if (df < de || (df == de && __ldg(recs + S.pos[f]).w < ie)) ++rank;
+            }
+        }
+        __syncwarp();
+        if (e < c && rank >= k) S.d2[e] = INT64_MAX;   // dropped by the compaction below
+        __syncwarp();
+    }
+    kw_compact(S, st, lane);
+}
+
+// Scan sorted positions [s, e): lane = candidate, hits appended to the buffer.
+template <int DIM>
+__device__ __forceinline__ void kw_scan(const int4* __restrict__ recs, int32_t s, int32_t e, const KwQuery<DIM>& q,
+                                        KwSh& S, KwState& st, int k, int lane) {
+    for (int32_t b = s; b < e; b += 32) {
+        const int32_t p = b + lane;
+        int64_t d = INT64_MAX;
+        bool hit = false;
+        if (p < e) {
+            const int4 r = __ldg(recs + p);
+            d = kw_d2<DIM>(q, r);
+            hit = d <= st.T && r.w != q.id;
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, hit);
+        if (m == 0) continue;
+        if (st.cnt + __popc(m) > KW_CAP) {
+            kw_select(S, st, k, lane);
+            kw_compact(S, st, lane);
+            if (st.cnt + 32 > KW_CAP) kw_keep_exact(recs, S, st, k, lane);
+            hit = hit && d <= st.T;
+            m = __ballot_sync(0xffffffffu, hit);
+        }
+        if (hit) {
+            const int slot = st.cnt + __popc(m & ((1u << lane) - 1u));
+            S.d2[slot] = d;
+            S.pos[slot] = p;
+        }
+        st.cnt += __popc(m);
+        __syncwarp();
+        if (st.cnt >= st.lim) {
+            // tighten T: at k buffered candidates (the first finite bound), then each
+            // time the buffer has grown by max(k, 32) since the last selection
+            kw_select(S, st, k, lane);
+            kw_compact(S, st, lane);
+            st.lim = min(st.cnt + max(k, 32), KW_CAP);
+        }
+    }
+}
+
+template <int DIM>
+__device__ __forceinline__ Node<DIM> kw_load_node(const Node<DIM>* p) {
+    Node<DIM> r;
+    const int4* s = reinterpret_cast<const int4*>(p);
+    int4* d = reinterpret_cast<int4*>(&r);
+#pragma unroll
+    for (int t = 0; t < (int)(sizeof(Node<DIM>) / 16); ++t) d[t] = __ldg(s + t);
+    return r;
+}
+
+// Alg. 2 searchDown of `cur` for one query (warp-uniform DFS; nearer child first,
+// reading 10; the far child waits on the stack with its box distance rounded down).
+template <int DIM>
+__device__ __forceinline__ void kw_down(const KwArgs& A, const Node<DIM>* __restrict__ nodes, Sub cur,
+                                        const KwQuery<DIM>& q, KwSh& S, KwState& st, int lane) {
+    int sp = 0;
+    while (true) {
+        bool descend = false;
+        if (cur.ref < 0) {
+            kw_scan<DIM>(A.recs, cur.s, cur.e, q, S, st, A.k, lane);
+        } else {
+            const Node<DIM> nd = kw_load_node<DIM>(nodes + cur.ref);
+            const int64_t dl = kw_boxd2<DIM>(q, nd.lbox), dr = kw_boxd2<DIM>(q, nd.rbox);
+            const bool ln = dl <= st.T, rn = dr <= st.T;
+            const Sub lc = sub_ref(nd.left, cur.s, nd.mid), rc = sub_ref(nd.right, nd.mid, cur.e);
+            if (ln && rn) {
+                const bool lfirst = dl <= dr;
+                const Sub far = lfirst ? rc : lc;
+                const float fd = __ll2float_rd(lfirst ? dr : dl);
+                ZD_DCHECK(sp < KW_STK);
+                __syncwarp();
+                if (lane == 0) S.stk[sp] = make_int4(far.ref, far.s, far.e, __float_as_int(fd));
+                ++sp;
+                cur = lfirst ? lc : rc;
+                descend = true;
+            } else if (ln || rn) {
+                cur = ln ? lc : rc;
+                descend = true;
+            }
+        }
+        if (descend) continue;
+        bool found = false;
+        __syncwarp();
+        while (sp > 0) {
+            const int4 e = S.stk[--sp];
+            // the stored value is <= the exact box d2: "> T" prunes soundly
+            if ((int64_t)__int_as_float(e.w) <= st.T) {
+                cur = Sub{e.x, e.y, e.z};
+                found = true;
+                break;
+            }
+        }
+        if (!found) break;
+    }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(KW_WARPS * 32, ZD_KW_MINB) knn_warp_kernel(KwArgs A) {
+    __shared__ KwSh sh[KW_WARPS];
+    const int lane = threadIdx.x & 31;
+    KwSh& S = sh[threadIdx.x >> 5];
+    const int64_t qi = (int64_t)blockIdx.x * KW_WARPS + (threadIdx.x >> 5);
+    if (qi >= A.nq) return;   // whole warp
+    const Node<DIM>* nodes = static_cast<const Node<DIM>*>(A.nodes);
+    const int4 r = __ldg(A.qrecs + qi);
+    KwQuery<DIM> q;
+    q.c[0] = r.x; q.c[1] = r.y; q.c[2] = r.z;
+    q.id = A.ext ? -1 : r.w;
+    KwState st{INT64_MAX, 0, A.k};
+
+    if (A.root_based) {
+        // Alg. 2 from the root with an empty list, no ascent
+        const int32_t root = __ldg(A.d_meta + 1);
+        kw_down<DIM>(A, nodes, root >= 0 ? sub_ref(root, 0, A.n_pts) : Sub{~0, 0, A.n_pts}, q, S, st, lane);
+    } else {
+        // Alg. 3: scan the query's leaf, then ascend; at each ancestor stop if the ball
+        // lies inside C's box, else search the sibling subtree
+        const int32_t l = __ldg(A.qleaf + qi);
+        kw_scan<DIM>(A.recs, __ldg(A.leaf_start + l), __ldg(A.leaf_start + l + 1), q, S, st, A.k, lane);
+        int32_t C = -1, P = __ldg(A.leaf_parent + l);
+        while (P >= 0) {
+            const Node<DIM> nd = kw_load_node<DIM>(nodes + P);
+            const bool isl = C >= 0 ? nd.left == C : P == l;   // leaf l is the left child of node l
+            const typename BoxT<DIM>::T* cb = isl ? nd.lbox : nd.rbox;
+            const typename BoxT<DIM>::T* sb = isl ? nd.rbox : nd.lbox;
+            if (kw_stop<DIM>(q, cb, st.T)) break;
+            if (kw_boxd2<DIM>(q, sb) <= st.T) {
+                const int2 pr = __ldg(A.pos_range + P);
+                kw_down<DIM>(A, nodes, isl ? sub_ref(nd.right, nd.mid, pr.y) : sub_ref(nd.left, pr.x, nd.mid), q, S,
+                             st, lane);
+            }
+            C = P;
+            P = nd.parent;
+        }
+    }
+
+    // final: trim to ~k, then rank exactly by (d2, id)
+    if (st.cnt > A.k) {
+        kw_select(S, st, A.k, lane);
+        kw_compact(S, st, lane);
+    }
+    const int c = st.cnt;
+    for (int e = lane; e < c; e += 32) S.pos[e] = __ldg(A.recs + S.pos[e]).w;
+    __syncwarp();
+    int64_t row;
+    if (A.ext) row = r.w;
+    else row = A.row_of_id ? __ldg(A.row_of_id + r.w) : r.w;
+    int32_t* oi = A.out_idx + row * A.k;
+    int64_t* od = A.out_d2 + row * A.k;
+    for (int e = lane; e < c; e += 32) {
+        const int64_t de = S.d2[e];
+        const int32_t ie = S.pos[e];
+        int rank = 0;
+        for (int f = 0; f < c; ++f) {
+            const int64_t df = S.d2[f];
+            rank += (df < de || (df == de && S.pos[f] < ie)) ? 1 : 0;
+        }
+        if (rank < A.k) { oi[rank] = ie; od[rank] = de; }
+    }
+    for (int t = c + lane; t < A.k; t += 32) { oi[t] = -1; od[t] = INT64_MAX; }
+}
+
+}  // namespace
+
+void knn_warp(const KnnArgs& a, const int4* qrecs, const int32_t* qleaf, int64_t nq, bool ext, cudaStream_t st) {
+    if (nq <= 0) return;
+    KwArgs A{};
+    A.recs = a.recs; A.leaf_start = a.leaf_start; A.leaf_parent = a.leaf_parent; A.nodes = a.nodes;
+    A.pos_range = a.pos_range; A.d_meta = a.d_meta; A.qrecs = qrecs; A.qleaf = qleaf;
+    A.nq = (int32_t)nq; A.n_pts = (int32_t)a.n; A.k = a.k; A.row_of_id = ext ? nullptr : a.row_of_id;
+    A.out_idx = a.out_idx; A.out_d2 = a.out_d2; A.ext = ext ? 1 : 0; A.root_based = a.root_based;
+    const int grid = (int)((nq + KW_WARPS - 1) / KW_WARPS);
+    count_launch(1);
+    if (a.dim == 2) knn_warp_kernel<2><<<grid, KW_WARPS * 32, 0, st>>>(A);
+    else knn_warp_kernel<3><<<grid, KW_WARPS * 32, 0, st>>>(A);
+}
+
+}  // namespace zd

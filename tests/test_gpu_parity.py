@@ -255,7 +255,7 @@ def test_errors(zd):
     after = t.zd_export()                            # all-or-nothing: unchanged
     assert np.array_equal(before["recs"], after["recs"]) and t.zd_size() == 1000
     assert t.zd_insert(dev(zdgen.uniform(1, 3, seed=4))) == 1000   # ids not consumed by the failed insert
-    for k in (0, 33):
+    for k in (0, zd.ZD_K_MAX + 1):
         with pytest.raises(zd.ZdError) as e:
             t.zd_knn(k)
         assert e.value.code == zd.ZD_EINVAL
@@ -313,3 +313,96 @@ def test_knn_root_based(zd, oracle_mod, dist, dim):
     torch.cuda.synchronize()
     oqi, oqd, _ = oracle_mod.Tree(pts).knn_queries(q, 10)
     check_rows(qi.cpu().numpy(), qd.cpu().numpy(), oqi, oqd)
+
+
+# ------------------------------------------------- large k (warp-per-query kernel)
+
+@pytest.mark.parametrize("dist,dim", [("uniform", 2), ("uniform", 3), ("plummer", 3), ("sphere", 3),
+                                      ("kuzmin", 2), ("dup", 2), ("dup", 3)])
+@pytest.mark.parametrize("k", [33, 64, 100, 128])
+def test_knn_large_k(zd, oracle_mod, dist, dim, k):
+    """k > 32 runs the warp-per-query kernel (knn_warp.cu; P:543's large-k container)."""
+    pts = zdgen.points(dist, 6000, dim, seed=13)
+    t = zd.zd_build(dev(pts))
+    gi, gd = gpu_knn_all(t, k)
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(k)
+    check_rows(gi, gd, oi, od)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 16, 17, 33, 1000, 5633])
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("k", [1, 10, 32])
+def test_knn_warp_forced_sizes(zd, oracle_mod, n, dim, k):
+    """The warp kernel forced for small k (ZD_KNN_WARP) on tiny and ragged sizes."""
+    pts = zdgen.uniform(n, dim, seed=200 + n)
+    t = zd.zd_build(dev(pts))
+    gi, gd = t.zd_knn(k, warp=True)
+    torch.cuda.synchronize()
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(k)
+    check_rows(gi.cpu().numpy(), gd.cpu().numpy(), oi, od)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("k", [10, 100])
+def test_knn_warp_far_corner_ties(zd, oracle_mod, dim, k):
+    pts = _far_corner_points(dim, seed=dim * 1000 + k)
+    t = zd.zd_build(dev(pts))
+    gi, gd = t.zd_knn(k, warp=True)
+    torch.cuda.synchronize()
+    bi, bd = oracle_mod.brute_knn(pts, None, pts, np.arange(len(pts), dtype=np.int32), k)
+    check_rows(gi.cpu().numpy(), gd.cpu().numpy(), bi, bd)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_knn_warp_massive_ties(zd, oracle_mod, dim):
+    """400 coincident copies of each of 6 sites: more equal distances than the warp
+    kernel's buffer holds, so the exact (d2, id) tie resolution runs."""
+    sites = zdgen.uniform(6, dim, seed=5)
+    pts = np.ascontiguousarray(np.repeat(sites, 400, axis=0))
+    t = zd.zd_build(dev(pts))
+    for k in (100, 128):
+        gi, gd = gpu_knn_all(t, k)
+        bi, bd = oracle_mod.brute_knn(pts, None, pts, np.arange(len(pts), dtype=np.int32), k)
+        check_rows(gi, gd, bi, bd)
+
+
+def test_knn_warp_lattice_every_row(zd, oracle_mod):
+    for side, dim in ((8, 3), (24, 2)):
+        pts = zdgen.grid(side, dim)
+        t = zd.zd_build(dev(pts))
+        for k in (57, 125):
+            gi, gd = gpu_knn_all(t, k)
+            bi, bd = oracle_mod.brute_knn(pts, None, pts, np.arange(len(pts), dtype=np.int32), k)
+            check_rows(gi, gd, bi, bd)
+
+
+@pytest.mark.parametrize("dist,dim", [("uniform", 3), ("plummer", 3), ("uniform", 2), ("dup", 2)])
+@pytest.mark.parametrize("k,warp", [(10, True), (64, False), (128, False)])
+def test_knn_warp_external_and_root(zd, oracle_mod, dist, dim, k, warp):
+    pts = zdgen.points(dist, 8000, dim, seed=41)
+    q = zdgen.uniform(1500, dim, seed=42)
+    if dist == "dup":
+        q = q % 8
+    t = zd.zd_build(dev(pts))
+    gi, gd = t.zd_knn(k, queries=dev(q), warp=warp)
+    torch.cuda.synchronize()
+    bi, bd = oracle_mod.brute_knn(pts, None, q, None, k)
+    check_rows(gi.cpu().numpy(), gd.cpu().numpy(), bi, bd)
+    ri, rd = t.zd_knn(k, root_based=True, warp=warp)
+    torch.cuda.synchronize()
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(k)
+    check_rows(ri.cpu().numpy(), rd.cpu().numpy(), oi, od)
+
+
+def test_knn_warp_after_updates(zd, oracle_mod):
+    base = zdgen.plummer(15000, 61)
+    t = zd.zd_build(dev(base))
+    live = oracle_mod.LiveSet(base)
+    b = zdgen.plummer(4000, 62)
+    assert t.zd_insert(dev(b)) == live.insert(b)
+    kill = zdgen.delete_ids(15000, 5000, seed=63)
+    assert t.zd_delete(dev(kill)) == live.delete(kill)
+    for k in (50, 128):
+        gi, gd = gpu_knn_all(t, k)
+        oi, od, _ = live.tree().knn_all(k)
+        check_rows(gi, gd, oi, od)
