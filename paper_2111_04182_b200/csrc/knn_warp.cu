@@ -116,8 +116,69 @@ __device__ __forceinline__ uint32_t kw_key(int64_t d2) { return __float_as_uint(
 struct KwState {
     int64_t T;
     int cnt;
-    int lim;   // re-select once cnt reaches this (first at k: the first finite bound)
+    int lim;     // re-select once cnt reaches this (first at k: the first finite bound)
+    float tf;    // ru(T) (INFINITY while T is INT64_MAX)
+    float wb;    // 3D fp32 box tests: exact box d2 <= T  =>  fp32 box d2 <= wb
 };
+
+__device__ __forceinline__ void kw_set_T(KwState& st, int64_t T) {
+    st.T = T;
+    st.tf = __ll2float_ru(T);
+    // the fp32 sum of three exact squares is at most (1 + 3.0000002 * 2^-24) times the
+    // exact one (as in knn.cu set_bound), so exact <= T implies fp32 <= wb
+    st.wb = __fmul_ru(st.tf, 1.0f + 0x1p-21f);
+}
+
+// Box distance in the test domain: fp32 in 3D (exact per-axis gaps), exact int64 in 2D.
+template <int DIM> struct KwBD { using T = int64_t; };
+template <> struct KwBD<3> { using T = float; };
+template <int DIM>
+__device__ __forceinline__ typename KwBD<DIM>::T kw_bd(const KwQuery<DIM>& q, const float* qf,
+                                                        const typename BoxT<DIM>::T* b) {
+    if constexpr (DIM == 3) {
+        float df = 0.f;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float t = fmaxf(b[a] - qf[a], 0.f) + fmaxf(qf[a] - b[3 + a], 0.f);
+            df = fmaf(t, t, df);
+        }
+        return df;
+    } else {
+        return kw_boxd2<DIM>(q, b);
+    }
+}
+template <int DIM>
+__device__ __forceinline__ bool kw_within(const KwState& st, typename KwBD<DIM>::T v) {
+    if constexpr (DIM == 3) return v <= st.wb;
+    else return v <= st.T;
+}
+// stack form of a box distance (fp32 bits): 3D the fp32 value itself; 2D rounded down
+template <int DIM>
+__device__ __forceinline__ int kw_bd_bits(typename KwBD<DIM>::T v) {
+    if constexpr (DIM == 3) return __float_as_int(v);
+    else return __float_as_int(__ll2float_rd(v));
+}
+template <int DIM>
+__device__ __forceinline__ bool kw_bits_within(const KwState& st, int bits) {
+    if constexpr (DIM == 3) return __int_as_float(bits) <= st.wb;
+    else return (int64_t)__int_as_float(bits) <= st.T;   // value <= exact box d2
+}
+// Alg. 3 stop test (reading 9) on C's box: 3D in fp32 — m exact, (m+1)^2 rounded down
+// against ru(T), so it never stops too early; 2D exact.
+template <int DIM>
+__device__ __forceinline__ bool kw_stop_t(const KwQuery<DIM>& q, const float* qf, const typename BoxT<DIM>::T* b,
+                                          const KwState& st) {
+    if constexpr (DIM == 3) {
+        float m = INFINITY;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) m = fminf(m, fminf(qf[a] - b[a], b[3 + a] - qf[a]));
+        if (m < 0.f) return false;
+        const float mm = m + 1.0f;
+        return __fmul_rd(mm, mm) > st.tf;
+    } else {
+        return kw_stop<DIM>(q, b, st.T);
+    }
+}
 
 // keep the buffered entries with d2 <= T (stable, in place: write index <= read index)
 __device__ __forceinline__ void kw_compact(KwSh& S, KwState& st, int lane) {
@@ -191,7 +252,7 @@ __device__ __forceinline__ void kw_select(KwSh& S, KwState& st, int k, int lane)
     }
     // an fp32 value >= 2^24 is an integer, and below 2^24 ru(d2) == d2: exact conversion
     const int64_t T = (int64_t)__uint_as_float(prefix);
-    if (T < st.T) st.T = T;
+    if (T < st.T) kw_set_T(st, T);
 }
 
 // Massive ties (rare): keep exactly the k best buffered entries by (d2, id).
@@ -214,6 +275,34 @@ __device__ __noinline__ void kw_keep_exact(const int4* __restrict__ recs, KwSh& 
         __syncwarp();
     }
     kw_compact(S, st, lane);
+}
+
+// Sort buf[0, c) ascending by (d2, id) (pos[] holds ids here; ids are distinct):
+// bitonic network over the next power of two >= c, padded with (INT64_MAX, INT_MAX).
+constexpr int kSortMax = 256;   // <= KW_CAP
+__device__ __forceinline__ void kw_sort(KwSh& S, int c, int lane) {
+    int P = 32;
+    while (P < c) P <<= 1;
+    for (int e = c + lane; e < P; e += 32) { S.d2[e] = INT64_MAX; S.pos[e] = INT_MAX; }
+    __syncwarp();
+#pragma unroll 1
+    for (int size = 2; size <= P; size <<= 1) {
+#pragma unroll 1
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = lane; t < (P >> 1); t += 32) {
+                const int i = 2 * stride * (t / stride) + (t % stride), j = i + stride;
+                const bool asc = (i & size) == 0;
+                const int64_t di = S.d2[i], dj = S.d2[j];
+                const int32_t pi = S.pos[i], pj = S.pos[j];
+                const bool gt = di > dj || (di == dj && pi > pj);
+                if (gt == asc) {
+                    S.d2[i] = dj; S.d2[j] = di;
+                    S.pos[i] = pj; S.pos[j] = pi;
+                }
+            }
+            __syncwarp();
+        }
+    }
 }
 
 // Scan sorted positions [s, e): lane = candidate, hits appended to the buffer.
@@ -269,7 +358,7 @@ __device__ __forceinline__ Node<DIM> kw_load_node(const Node<DIM>* p) {
 // reading 10; the far child waits on the stack with its box distance rounded down).
 template <int DIM>
 __device__ __forceinline__ void kw_down(const KwArgs& A, const Node<DIM>* __restrict__ nodes, Sub cur,
-                                        const KwQuery<DIM>& q, KwSh& S, KwState& st, int lane) {
+                                        const KwQuery<DIM>& q, const float* qf, KwSh& S, KwState& st, int lane) {
     int sp = 0;
     while (true) {
         bool descend = false;
@@ -277,16 +366,16 @@ __device__ __forceinline__ void kw_down(const KwArgs& A, const Node<DIM>* __rest
             kw_scan<DIM>(A.recs, cur.s, cur.e, q, S, st, A.k, lane);
         } else {
             const Node<DIM> nd = kw_load_node<DIM>(nodes + cur.ref);
-            const int64_t dl = kw_boxd2<DIM>(q, nd.lbox), dr = kw_boxd2<DIM>(q, nd.rbox);
-            const bool ln = dl <= st.T, rn = dr <= st.T;
+            const typename KwBD<DIM>::T dl = kw_bd<DIM>(q, qf, nd.lbox), dr = kw_bd<DIM>(q, qf, nd.rbox);
+            const bool ln = kw_within<DIM>(st, dl), rn = kw_within<DIM>(st, dr);
             const Sub lc = sub_ref(nd.left, cur.s, nd.mid), rc = sub_ref(nd.right, nd.mid, cur.e);
             if (ln && rn) {
                 const bool lfirst = dl <= dr;
                 const Sub far = lfirst ? rc : lc;
-                const float fd = __ll2float_rd(lfirst ? dr : dl);
+                const int fb = kw_bd_bits<DIM>(lfirst ? dr : dl);
                 ZD_DCHECK(sp < KW_STK);
                 __syncwarp();
-                if (lane == 0) S.stk[sp] = make_int4(far.ref, far.s, far.e, __float_as_int(fd));
+                if (lane == 0) S.stk[sp] = make_int4(far.ref, far.s, far.e, fb);
                 ++sp;
                 cur = lfirst ? lc : rc;
                 descend = true;
@@ -300,8 +389,7 @@ __device__ __forceinline__ void kw_down(const KwArgs& A, const Node<DIM>* __rest
         __syncwarp();
         while (sp > 0) {
             const int4 e = S.stk[--sp];
-            // the stored value is <= the exact box d2: "> T" prunes soundly
-            if ((int64_t)__int_as_float(e.w) <= st.T) {
+            if (kw_bits_within<DIM>(st, e.w)) {
                 cur = Sub{e.x, e.y, e.z};
                 found = true;
                 break;
@@ -323,12 +411,13 @@ __global__ void __launch_bounds__(KW_WARPS * 32, ZD_KW_MINB) knn_warp_kernel(KwA
     KwQuery<DIM> q;
     q.c[0] = r.x; q.c[1] = r.y; q.c[2] = r.z;
     q.id = A.ext ? -1 : r.w;
-    KwState st{INT64_MAX, 0, A.k};
+    KwState st{INT64_MAX, 0, A.k, INFINITY, INFINITY};
+    const float qf[3] = {(float)r.x, (float)r.y, (float)r.z};   // exact (3D: < 2^21)
 
     if (A.root_based) {
         // Alg. 2 from the root with an empty list, no ascent
         const int32_t root = __ldg(A.d_meta + 1);
-        kw_down<DIM>(A, nodes, root >= 0 ? sub_ref(root, 0, A.n_pts) : Sub{~0, 0, A.n_pts}, q, S, st, lane);
+        kw_down<DIM>(A, nodes, root >= 0 ? sub_ref(root, 0, A.n_pts) : Sub{~0, 0, A.n_pts}, q, qf, S, st, lane);
     } else {
         // Alg. 3: scan the query's leaf, then ascend; at each ancestor stop if the ball
         // lies inside C's box, else search the sibling subtree
@@ -340,11 +429,11 @@ __global__ void __launch_bounds__(KW_WARPS * 32, ZD_KW_MINB) knn_warp_kernel(KwA
             const bool isl = C >= 0 ? nd.left == C : P == l;   // leaf l is the left child of node l
             const typename BoxT<DIM>::T* cb = isl ? nd.lbox : nd.rbox;
             const typename BoxT<DIM>::T* sb = isl ? nd.rbox : nd.lbox;
-            if (kw_stop<DIM>(q, cb, st.T)) break;
-            if (kw_boxd2<DIM>(q, sb) <= st.T) {
+            if (kw_stop_t<DIM>(q, qf, cb, st)) break;
+            if (kw_within<DIM>(st, kw_bd<DIM>(q, qf, sb))) {
                 const int2 pr = __ldg(A.pos_range + P);
-                kw_down<DIM>(A, nodes, isl ? sub_ref(nd.right, nd.mid, pr.y) : sub_ref(nd.left, pr.x, nd.mid), q, S,
-                             st, lane);
+                kw_down<DIM>(A, nodes, isl ? sub_ref(nd.right, nd.mid, pr.y) : sub_ref(nd.left, pr.x, nd.mid), q, qf,
+                             S, st, lane);
             }
             C = P;
             P = nd.parent;
@@ -356,25 +445,36 @@ __global__ void __launch_bounds__(KW_WARPS * 32, ZD_KW_MINB) knn_warp_kernel(KwA
         kw_select(S, st, A.k, lane);
         kw_compact(S, st, lane);
     }
+    if (st.cnt > kSortMax) kw_keep_exact(A.recs, S, st, A.k, lane);   // massive ties: exactly k left
     const int c = st.cnt;
-    for (int e = lane; e < c; e += 32) S.pos[e] = __ldg(A.recs + S.pos[e]).w;
-    __syncwarp();
+    for (int e = lane; e < c; e += 32) S.pos[e] = __ldg(A.recs + S.pos[e]).w;   // positions -> ids
     int64_t row;
     if (A.ext) row = r.w;
     else row = A.row_of_id ? __ldg(A.row_of_id + r.w) : r.w;
     int32_t* oi = A.out_idx + row * A.k;
     int64_t* od = A.out_d2 + row * A.k;
-    for (int e = lane; e < c; e += 32) {
-        const int64_t de = S.d2[e];
-        const int32_t ie = S.pos[e];
-        int rank = 0;
-        for (int f = 0; f < c; ++f) {
-            const int64_t df = S.d2[f];
-            rank += (df < de || (df == de && S.pos[f] < ie)) ? 1 : 0;
+    if (c <= 32) {
+        // one survivor per lane: its rank by counting (c steps)
+        __syncwarp();
+        if (lane < c) {
+            const int64_t de = S.d2[lane];
+            const int32_t ie = S.pos[lane];
+            int rank = 0;
+            for (int f = 0; f < c; ++f) {
+                const int64_t df = S.d2[f];
+                rank += (df < de || (df == de && S.pos[f] < ie)) ? 1 : 0;
+            }
+            if (rank < A.k) { oi[rank] = ie; od[rank] = de; }
         }
-        if (rank < A.k) { oi[rank] = ie; od[rank] = de; }
+        for (int t = c + lane; t < A.k; t += 32) { oi[t] = -1; od[t] = INT64_MAX; }
+    } else {
+        kw_sort(S, c, lane);
+        for (int t = lane; t < A.k; t += 32) {
+            const bool v = t < c;
+            oi[t] = v ? S.pos[t] : -1;
+            od[t] = v ? S.d2[t] : INT64_MAX;
+        }
     }
-    for (int t = c + lane; t < A.k; t += 32) { oi[t] = -1; od[t] = INT64_MAX; }
 }
 
 }  // namespace
