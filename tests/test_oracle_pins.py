@@ -229,7 +229,7 @@ def numpy_brute(points, qrows, k, ids=None):
 def test_brute_vs_numpy(oracle_mod, dist, dim):
     pts = zdgen.points(dist, 700, dim, seed=4)
     rows = np.arange(0, 700, 7)
-    for k in (1, 5, 12):
+    for k in (1, 5, 12, 128):
         oi, od = oracle_mod.brute_knn(pts, None, pts[rows], rows.astype(np.int32), k)
         ni, nd = numpy_brute(pts, rows, k)
         assert np.array_equal(oi, ni) and np.array_equal(od, nd)
@@ -251,7 +251,7 @@ CASES = [("uniform", 2, 3000), ("uniform", 3, 3000), ("plummer", 3, 3000), ("sph
 
 
 @pytest.mark.parametrize("dist,dim,n", CASES)
-@pytest.mark.parametrize("k", [1, 5, 10, 100])
+@pytest.mark.parametrize("k", [1, 5, 10, 100, 128])
 def test_tree_knn_equals_brute(oracle_mod, dist, dim, n, k):
     pts = zdgen.points(dist, n, dim, seed=17)
     t = oracle_mod.Tree(pts)
