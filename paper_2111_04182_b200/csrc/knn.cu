@@ -145,7 +145,10 @@ struct Pw {
 #ifndef ZD_MINB
 #define ZD_MINB 7         // min resident blocks per SM for K <= 10 (register budget)
 #endif
-constexpr int CH = 16;                   // candidates tested per uniform pass
+#ifndef ZD_CH
+#define ZD_CH 16
+#endif
+constexpr int CH = ZD_CH;                // candidates tested per uniform pass
 constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
 #ifndef ZD_STK
 #define ZD_STK kMaxDepth
@@ -194,6 +197,9 @@ __device__ __forceinline__ Ref right_child(const Node<DIM>& nd, int32_t e) { ret
 #ifndef ZD_F32FILTER
 #define ZD_F32FILTER 1   // 3D: candidate tests in fp32 (exact coordinates), confirmed in int64
 #endif
+#if !ZD_F32FILTER
+#error "the 3D path requires ZD_F32FILTER (fp32 staged candidates)"
+#endif
 #ifndef ZD_PREFILTER
 #define ZD_PREFILTER 1   // drop staged candidates outside the packet box dilated by the span's max bound
 #endif
@@ -201,6 +207,9 @@ __device__ __forceinline__ Ref right_child(const Node<DIM>& nd, int32_t e) { ret
 #define ZD_PREGROUPS 1   // prefilter boxes per packet (groups of 32 / G Morton-consecutive lanes)
 #endif
 constexpr int kPG = ZD_PREGROUPS, kPGW = 32 / ZD_PREGROUPS;
+#ifndef ZD_FIXED_PASS
+#define ZD_FIXED_PASS 1  // uniform passes test exactly CH staged slots (masked), self excluded on hits
+#endif
 #ifndef ZD_PREFILTER2D
 #define ZD_PREFILTER2D 0 // the same in 2D (exact int64; measured slightly slower on C2 / 2D Kuzmin)
 #endif
@@ -450,8 +459,29 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
             uint32_t hit = 0;
             if (w > TMax<DIM>::v) {
                 // every lane tests every candidate against its own bound
-#if ZD_F32FILTER
-                if (DIM == 3) {
+#if ZD_FIXED_PASS
+                // fixed CH-wide pass (no trip-count checks); slots past cnt hold stale
+                // values and are masked off; self is excluded on the hit path
+                if constexpr (DIM == 3) {
+                    const float wb = L.wb;
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) {
+                        const float4 c = S.f[h0 + j];
+                        const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
+                        const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                        if (df <= wb) hit |= 1u << j;
+                    }
+                } else {
+                    const int64_t U = L.U;
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) {
+                        const int4 c = S.c[h0 + j];
+                        if (dist2<DIM>(L.q, c) <= U) hit |= 1u << j;
+                    }
+                }
+                hit &= cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+#else
+                if constexpr (DIM == 3) {
                     const float wb = L.wb;
 #pragma unroll kUnroll
                     for (int j = 0; j < cnt; ++j) {
@@ -461,9 +491,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                         const bool h = df <= wb && __float_as_int(c.w) != L.q.id;   // self excluded by id
                         hit |= (h ? 1u : 0u) << j;
                     }
-                } else
-#endif
-                {
+                } else {
                     const int64_t U = L.U;
 #pragma unroll kUnroll
                     for (int j = 0; j < cnt; ++j) {
@@ -472,6 +500,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                         hit |= (h ? 1u : 0u) << j;
                     }
                 }
+#endif
             } else {
                 // few lanes need these candidates: lane j holds candidate j and the warp
                 // loops over the needing queries (broadcast by shuffle), one ballot each
@@ -531,13 +560,15 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                     const float4 c = S.f[j];
                     const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
                     const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                    if (df > L.wb) continue;   // the bound shrank since the test
+                    // the bound shrank since the test, or self (excluded by id, reading 13)
+                    if (df > L.wb || __float_as_int(c.w) == L.q.id) continue;
                     xf = __fmul_ru(df, 1.0f + 0x1p-21f);   // >= the exact d2
                 } else
 #endif
                 {
-                    const int64_t d = dist2<DIM>(L.q, S.c[j]);
-                    if (d > L.U) continue;   // the bound shrank since the test
+                    const int4 c = S.c[j];
+                    const int64_t d = dist2<DIM>(L.q, c);
+                    if (d > L.U || c.w == L.q.id) continue;   // bound shrank since the test, or self
                     xf = __ll2float_ru(d);
                 }
                 // sorted insertion of xf, dropping the largest: every new slot is the
