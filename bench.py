@@ -249,13 +249,21 @@ def alu_ops_per_query(per_q: dict) -> float:
 
 
 def load_traffic():
-    """Per-launch DRAM bytes of the main k-NN kernel (the longest captured launch) from
-    the newest committed ncu summary under profiles/, if any."""
-    files = sorted((ROOT / "profiles").glob("*ncu_knn*.json"), key=lambda p: p.stat().st_mtime, reverse=True)
-    for p in files:
+    """Per-launch DRAM bytes of the bench's k-NN kernel (the packet kernel at k=10, its
+    longest captured launch) from the newest committed `rNN_ncu_knn_vMM.json` summary
+    under profiles/ (highest round, then version; file times are not trusted)."""
+    import re
+    pat = re.compile(r"r(\d+)_ncu_knn_v(\d+)\.json$")
+    files = []
+    for p in (ROOT / "profiles").glob("r*_ncu_knn_v*.json"):
+        m = pat.search(p.name)
+        if m:
+            files.append(((int(m.group(1)), int(m.group(2))), p))
+    for _, p in sorted(files, reverse=True):
         try:
             d = json.loads(p.read_text())
-            ks = [k for k in d.get("kernels", []) if "dram_bytes_per_launch" in k]
+            ks = [k for k in d.get("kernels", []) if "dram_bytes_per_launch" in k
+                  and "knn_packet_kernel<3, 10" in k.get("kernel", "").replace("(int)", "")]
             if not ks:
                 continue
             main = max(ks, key=lambda k: k.get("gpu__time_duration.sum", [0])[0])
@@ -412,7 +420,7 @@ def run_gpu(args, D: Dist):
         "insert_mpts_s": c["insert_m"] / (mean_ph[1] / 1e3) / 1e6,
         "delete_mpts_s": c["delete_m"] / (mean_ph[2] / 1e3) / 1e6,
         "knn_qps": n_live / (mean_ph[3] / 1e3),
-        "roofline": {"kernel": "knn_all_kernel<3,10>", "bound": "alu", "achieved": achieved, "peak": peak,
+        "roofline": {"kernel": "knn_packet_kernel<3,10>", "bound": "alu", "achieved": achieved, "peak": peak,
                      "unit": "Tops/s (int32 lane-ops)", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src,
                      "ops_per_query": ops_q, "counters_per_query": per_q,
