@@ -143,7 +143,10 @@ struct Pw {
     static constexpr int v = K <= 16 ? ZD_PW : 2;   // warps per block (shared memory grows with K)
 };
 #ifndef ZD_MINB
-#define ZD_MINB 7         // min resident blocks per SM for K <= 10 (register budget)
+#define ZD_MINB 7         // 2D: min resident blocks per SM for K <= 10 (register budget)
+#endif
+#ifndef ZD_MINB3
+#define ZD_MINB3 8        // 3D (64 registers; with Cap 20 the shared memory fits 8 blocks)
 #endif
 #ifndef ZD_CH
 #define ZD_CH 16
@@ -159,11 +162,15 @@ constexpr int kStk = ZD_STK;             // per-warp stack entries (>= tree heig
 #define ZD_MINB16 5       // min resident blocks per SM for 10 < K <= 16
 #endif
 #ifndef ZD_CAP_MIN
-#define ZD_CAP_MIN 22
+#define ZD_CAP_MIN 22     // 2D
 #endif
-template <int K>
+#ifndef ZD_CAP_MIN3
+#define ZD_CAP_MIN3 20    // 3D
+#endif
+template <int DIM, int K>
 struct Cap {   // buffered candidates per lane (overflow compacts per lane: any value > K works)
-    static constexpr int v = (K + 8 > ZD_CAP_MIN) ? K + 8 : ZD_CAP_MIN;
+    static constexpr int cm = DIM == 3 ? ZD_CAP_MIN3 : ZD_CAP_MIN;
+    static constexpr int v = (K + 8 > cm) ? K + 8 : cm;
 };
 
 // A child reference in traversal form: ref >= 0 internal node; ref < 0 a leaf with
@@ -213,16 +220,16 @@ constexpr int kPG = ZD_PREGROUPS, kPGW = 32 / ZD_PREGROUPS;
 #ifndef ZD_PREFILTER2D
 #define ZD_PREFILTER2D 0 // the same in 2D (exact int64; measured slightly slower on C2 / 2D Kuzmin)
 #endif
-template <int K>
+template <int DIM, int K>
 struct WarpSh {
-    int4 c[32];                          // staged candidates (x, y, z|0, id)
+    int4 c[DIM == 2 ? 32 : 1];           // 2D: staged candidates (x, y, 0, id)
 #if ZD_F32FILTER
     float4 f[32];                        // 3D: the same in fp32 (exact below 2^24)
 #endif
     int32_t p[32];                       // their sorted positions
     float4 pb[2 * kPG];                  // query box of each lane group (lo, hi; 2D: int bits)
-    int32_t bp[Cap<K>::v][32];           // per-lane buffered positions; column = lane
-    float bf[Cap<K>::v][32];             //   ... and their d2 rounded up to fp32
+    int32_t bp[Cap<DIM, K>::v][32];           // per-lane buffered positions; column = lane
+    float bf[Cap<DIM, K>::v][32];             //   ... and their d2 rounded up to fp32
     int4 stk[kStk];                      // (ref, s, e, parent | side << 31): box reloaded on pop
 #ifdef ZD_DEBUG
     int32_t dbg_npts, dbg_nint;          // bounds for ZD_DCHECK
@@ -314,7 +321,7 @@ __device__ __forceinline__ bool lane_stop(const Lane<DIM, K>& L, const typename 
 // Drop buffered candidates that can no longer qualify: a final neighbour p has
 // d2(p) <= the exact k-th smallest d2 seen so far, hence ru(d2(p)) <= fa[K-1].
 template <int DIM, int K>
-__device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
+__device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<DIM, K>& S, int lane) {
     // 3D buffers fp32-derived upper bounds ub with d2 <= ub <= d2 (1 + 2^-20): a final
     // neighbour has ub <= D_k (1 + 2^-20) <= fa[K-1] (1 + 2^-20)
     const float F = DIM == 3 ? __fmul_ru(L.fa[K - 1], 1.0f + 0x1p-20f) : L.fa[K - 1];
@@ -334,7 +341,7 @@ __device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<K>& S, int lane)
 // by the next compaction; the K kept ones all have ru(d2) <= fa[K-1], so later
 // compactions keep them.  (Arguments by value: no Lane round trip through memory.)
 template <int DIM, int K>
-__device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Query<DIM> q, int cnt, WarpSh<K>& S,
+__device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Query<DIM> q, int cnt, WarpSh<DIM, K>& S,
                                                int lane) {
     for (int e = 0; e < cnt; ++e) {
         const int4 ce = __ldg(recs + S.bp[e][lane]);
@@ -367,7 +374,7 @@ struct TMax {
 };
 template <int DIM, int K>
 __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t s, int32_t e, bool need,
-                                          Lane<DIM, K>& L, WarpSh<K>& S, int lane) {
+                                          Lane<DIM, K>& L, WarpSh<DIM, K>& S, int lane) {
     const uint32_t M = __ballot_sync(0xffffffffu, need);
     if (M == 0) return;
     const int w = __popc(M);
@@ -441,7 +448,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
         if (n32 == 0) continue;
         if (keep) {
             const int slot = __popc(km & ((1u << lane) - 1u));
-            S.c[slot] = r;
+            if constexpr (DIM == 2) S.c[slot] = r;
             S.p[slot] = b + lane;
 #if ZD_F32FILTER
             if (DIM == 3) S.f[slot] = fc;
@@ -452,7 +459,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
             const int cnt = min(CH, n32 - h0);
             // compact (all lanes together) once some needing lane is nearly full; a lane
             // that still fills up while taking hits compacts on its own (take_hit)
-            if (__any_sync(0xffffffffu, need && L.cnt > Cap<K>::v - ZD_SLACK)) {
+            if (__any_sync(0xffffffffu, need && L.cnt > Cap<DIM, K>::v - ZD_SLACK)) {
                 ZD_STAT(ZS_COMPACT, 1);
                 compact<DIM, K>(L, S, lane);
             }
@@ -506,8 +513,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 // loops over the needing queries (broadcast by shuffle), one ballot each
                 const bool cv = lane < cnt;
                 uint32_t m = M;
-#if ZD_F32FILTER
-                if (DIM == 3) {
+                if constexpr (DIM == 3) {
                     const float4 c = S.f[h0 + (cv ? lane : 0)];
                     while (m) {
                         const int i = __ffs(m) - 1;
@@ -523,22 +529,21 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                         const uint32_t B = __ballot_sync(0xffffffffu, h);
                         if (lane == i) hit = B;
                     }
-                    m = 0;
-                }
-#endif
-                const int4 c = S.c[h0 + (cv ? lane : 0)];
-                while (m) {
-                    const int i = __ffs(m) - 1;
-                    m &= m - 1;
-                    Query<DIM> qi;
-                    qi.c[0] = __shfl_sync(0xffffffffu, L.q.c[0], i);
-                    qi.c[1] = __shfl_sync(0xffffffffu, L.q.c[1], i);
-                    qi.c[2] = DIM == 3 ? __shfl_sync(0xffffffffu, L.q.c[2], i) : 0;
-                    const int32_t idi = __shfl_sync(0xffffffffu, L.q.id, i);
-                    const int64_t Ui = __shfl_sync(0xffffffffu, L.U, i);
-                    const bool h = cv && dist2<DIM>(qi, c) <= Ui && c.w != idi;
-                    const uint32_t B = __ballot_sync(0xffffffffu, h);
-                    if (lane == i) hit = B;
+                } else {
+                    const int4 c = S.c[h0 + (cv ? lane : 0)];
+                    while (m) {
+                        const int i = __ffs(m) - 1;
+                        m &= m - 1;
+                        Query<DIM> qi;
+                        qi.c[0] = __shfl_sync(0xffffffffu, L.q.c[0], i);
+                        qi.c[1] = __shfl_sync(0xffffffffu, L.q.c[1], i);
+                        qi.c[2] = 0;
+                        const int32_t idi = __shfl_sync(0xffffffffu, L.q.id, i);
+                        const int64_t Ui = __shfl_sync(0xffffffffu, L.U, i);
+                        const bool h = cv && dist2<DIM>(qi, c) <= Ui && c.w != idi;
+                        const uint32_t B = __ballot_sync(0xffffffffu, h);
+                        if (lane == i) hit = B;
+                    }
                 }
             }
 #ifdef ZD_KNN_STATS
@@ -555,17 +560,14 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 const int j = h0 + __ffs(hit) - 1;
                 hit &= hit - 1;
                 float xf;
-#if ZD_F32FILTER
-                if (DIM == 3) {
+                if constexpr (DIM == 3) {
                     const float4 c = S.f[j];
                     const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
                     const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                     // the bound shrank since the test, or self (excluded by id, reading 13)
                     if (df > L.wb || __float_as_int(c.w) == L.q.id) continue;
                     xf = __fmul_ru(df, 1.0f + 0x1p-21f);   // >= the exact d2
-                } else
-#endif
-                {
+                } else {
                     const int4 c = S.c[j];
                     const int64_t d = dist2<DIM>(L.q, c);
                     if (d > L.U || c.w == L.q.id) continue;   // bound shrank since the test, or self
@@ -578,14 +580,14 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 for (int t = K - 1; t > 0; --t) L.fa[t] = fmaxf(L.fa[t - 1], fminf(L.fa[t], xf));
                 L.fa[0] = fminf(L.fa[0], xf);
                 set_bound<DIM, K>(L);
-                if (L.cnt == Cap<K>::v) {   // rare: per-lane compaction
+                if (L.cnt == Cap<DIM, K>::v) {   // rare: per-lane compaction
                     compact<DIM, K>(L, S, lane);
-                    if (L.cnt == Cap<K>::v) {   // massive ties: keep only the exact K best
+                    if (L.cnt == Cap<DIM, K>::v) {   // massive ties: keep only the exact K best
                         mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
                         compact<DIM, K>(L, S, lane);
                     }
                 }
-                ZD_DCHECK(L.cnt < Cap<K>::v);
+                ZD_DCHECK((L.cnt < Cap<DIM, K>::v));
                 S.bp[L.cnt][lane] = S.p[j];
                 S.bf[L.cnt][lane] = xf;
                 ++L.cnt;
@@ -600,7 +602,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
 template <int DIM, int K>
 __device__ __forceinline__ void scan_leaves(const int4* __restrict__ recs, int32_t s, int32_t mid, int32_t e,
                                             bool needl, bool needr, int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L,
-                                            WarpSh<K>& S, int lane) {
+                                            WarpSh<DIM, K>& S, int lane) {
     const int32_t a1 = min(e, max(s, ps_lo));   // piece before the scanned span: [s, a1)
     const int32_t b0 = max(s, min(e, ps_hi));   // piece after it: [b0, e)
     // one inlined copy of scan_span for both pieces (code size: the I-cache matters)
@@ -617,7 +619,7 @@ __device__ __forceinline__ void scan_leaves(const int4* __restrict__ recs, int32
 template <int DIM, int K>
 __device__ __forceinline__ void joint_down(const int4* __restrict__ recs, const Node<DIM>* __restrict__ nodes, Ref cur,
                                            bool cur_need, int32_t ps_lo, int32_t ps_hi, Lane<DIM, K>& L,
-                                           WarpSh<K>& S, int lane) {
+                                           WarpSh<DIM, K>& S, int lane) {
     int sp = 0;
     while (true) {
         bool descend = false, scan = false;
@@ -735,7 +737,7 @@ struct PacketArgs {
 // Returns false (writing nothing) if the packet was deferred to the second pass.
 template <int DIM, int K, bool EXT>
 __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, int32_t pe, int64_t pk, bool can_defer,
-                                              WarpSh<K>& S, int lane) {
+                                              WarpSh<DIM, K>& S, int lane) {
     const int32_t p = p0 + lane;
     const bool active = p < pe;
     const int32_t pq = active ? p : p0;
@@ -964,11 +966,11 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
 }
 
 template <int DIM, int K, bool EXT>
-__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? ZD_MINB : (K <= 16 ? ZD_MINB16 : 2))) knn_packet_kernel(PacketArgs A) {
+__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? (DIM == 3 ? ZD_MINB3 : ZD_MINB) : (K <= 16 ? ZD_MINB16 : 2))) knn_packet_kernel(PacketArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpSh<K>* sh = reinterpret_cast<WarpSh<K>*>(smem_raw);   // Pw<K>::v warps
+    WarpSh<DIM, K>* sh = reinterpret_cast<WarpSh<DIM, K>*>(smem_raw);   // Pw<K>::v warps
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    WarpSh<K>& S = sh[wib];
+    WarpSh<DIM, K>& S = sh[wib];
 #ifdef ZD_DEBUG
     if (lane == 0) {
         S.dbg_nint = __ldg(A.d_meta);
@@ -1030,7 +1032,7 @@ void launch_packets(const PacketArgs& A, cudaStream_t st) {
     const int64_t warps = ((int64_t)A.nq + 31) / 32;
     const int grid = (int)((warps + Pw<K>::v - 1) / Pw<K>::v);
     if (grid <= 0) return;
-    const size_t smem = sizeof(WarpSh<K>) * Pw<K>::v;
+    const size_t smem = sizeof(WarpSh<DIM, K>) * Pw<K>::v;
     static bool attr_set = false;   // per template instance
     if (!attr_set) {
         cudaFuncSetAttribute(knn_packet_kernel<DIM, K, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
