@@ -136,6 +136,7 @@ struct zd_tree {
     int dim = 3, leaf_max = 16;
     cudaStream_t st = nullptr;
     int64_t n = 0, n_next = 0, cap = 0, id_cap = 0;
+    int64_t ncap = 0;   // internal-node capacity of the node-indexed tree buffers
     // sorted live points
     uint64_t* keys = nullptr;
     int4* recs = nullptr;
@@ -171,24 +172,51 @@ void free_tree_bufs(zd_tree* h) {
     dfree(t.split_bit, h->st); dfree(t.visit, h->st); dfree(t.range, h->st); dfree(t.pos_range, h->st);
     dfree(t.flags, h->st); dfree(t.block_cnt, h->st);
     if (t.nodes) { cudaFreeAsync(t.nodes, h->st); t.nodes = nullptr; }
+    h->ncap = 0;
+}
+
+// Node-indexed buffers (internal nodes <= ncap, leaves <= ncap + 1).
+void free_node_bufs(zd_tree* h) {
+    TreeBufs& t = h->tb;
+    dfree(t.leaf_start, h->st); dfree(t.leaf_parent, h->st); dfree(t.split_bit, h->st);
+    dfree(t.visit, h->st); dfree(t.range, h->st); dfree(t.pos_range, h->st);
+    if (t.nodes) { cudaFreeAsync(t.nodes, h->st); t.nodes = nullptr; }
+    h->ncap = 0;
+}
+int alloc_node_bufs(zd_tree* h, int64_t ncap) {
+    free_node_bufs(h);
+    TreeBufs& t = h->tb;
+    ncap = std::max<int64_t>(ncap, 1);
+    const size_t node_bytes = h->dim == 2 ? 48 : 64;
+    ZD_CUDA(dalloc(&t.leaf_start, ncap + 2, h->st));
+    ZD_CUDA(dalloc(&t.leaf_parent, ncap + 1, h->st));
+    ZD_CUDA(dalloc(&t.split_bit, ncap, h->st));
+    ZD_CUDA(dalloc(&t.visit, ncap, h->st));
+    ZD_CUDA(dalloc(&t.range, 2 * ncap, h->st));
+    ZD_CUDA(dalloc(&t.pos_range, ncap, h->st));
+    ZD_CUDA(cudaMallocAsync(&t.nodes, ncap * node_bytes, h->st));
+    h->ncap = ncap;
+    return ZD_OK;
+}
+
+// Below this many points the node buffers are sized for the worst case (n - 1
+// internal nodes) and the topology needs no host round trip; above it they are sized
+// from the node count of each build (one sync after the flag scan), so the tree takes
+// ~14 B/pt instead of ~100 (3D, leaf size 16) and 10^9 points fit in 180 GB.
+// ZD_EXACT_NODES_MIN (testing) overrides the threshold.
+int64_t exact_nodes_min() {
+    if (const char* e = std::getenv("ZD_EXACT_NODES_MIN")) return std::atoll(e);
+    return (int64_t)1 << 25;
 }
 
 int alloc_tree_bufs(zd_tree* h, int64_t cap) {
     free_tree_bufs(h);
     TreeBufs& t = h->tb;
     t.d_meta = h->d_small;
-    const size_t node_bytes = h->dim == 2 ? 48 : 64;
     ZD_CUDA(dalloc(&t.pt_leaf, cap, h->st));
-    ZD_CUDA(dalloc(&t.leaf_start, cap + 2, h->st));
-    ZD_CUDA(dalloc(&t.leaf_parent, cap + 1, h->st));
-    ZD_CUDA(dalloc(&t.split_bit, cap, h->st));
-    ZD_CUDA(dalloc(&t.visit, cap, h->st));
-    ZD_CUDA(dalloc(&t.range, 2 * cap, h->st));
-    ZD_CUDA(dalloc(&t.pos_range, cap, h->st));
     ZD_CUDA(dalloc(&t.flags, cap, h->st));
     ZD_CUDA(dalloc(&t.block_cnt, std::max(tree_blocks(cap), compact_blocks(cap)) + 2, h->st));
-    ZD_CUDA(cudaMallocAsync(&t.nodes, std::max<int64_t>(cap, 1) * node_bytes, h->st));
-    return ZD_OK;
+    return alloc_node_bufs(h, cap <= exact_nodes_min() ? cap : cap / 8);
 }
 
 // Point capacity for keys/recs (and their alternates) + tree buffers.
@@ -236,19 +264,30 @@ int ensure_id_cap(zd_tree* h, int64_t need) {
 }
 
 // Sorted (keys, recs) of n points with ids id_base.. into the given outputs.
-int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out) {
+// use_alt: the ping-pong buffers live in the idle update alternates keys2/recs2
+// (8 + 16 bytes per point = 2 x (u64 key + u32 id)); else they are allocated.
+int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
+              bool use_alt = false) {
     if (n <= 0) return ZD_OK;
     SortScratch s{};
-    ZD_CUDA(dalloc(&s.k[0], n, h->st));
-    ZD_CUDA(dalloc(&s.k[1], n, h->st));
-    ZD_CUDA(dalloc(&s.v[0], n, h->st));
-    ZD_CUDA(dalloc(&s.v[1], n, h->st));
+    const bool alt = use_alt && h->keys2 && h->recs2 && n <= h->cap;
+    if (alt) {
+        s.k[0] = h->keys2;
+        s.k[1] = reinterpret_cast<uint64_t*>(h->recs2);
+        s.v[0] = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(h->recs2) + (size_t)n * sizeof(uint64_t));
+        s.v[1] = s.v[0] + n;
+    } else {
+        ZD_CUDA(dalloc(&s.k[0], n, h->st));
+        ZD_CUDA(dalloc(&s.k[1], n, h->st));
+        ZD_CUDA(dalloc(&s.v[0], n, h->st));
+        ZD_CUDA(dalloc(&s.v[1], n, h->st));
+    }
     s.zero_words = sort_zero_words(n);
     ZD_CUDA(dalloc(&s.zero_block, s.zero_words, h->st));
     ZD_CUDA(dalloc(&s.offs, 8 * 256, h->st));
     sort_points(h->dim, dpts, n, id_base, keys_out, recs_out, s, d_invalid(h), h->st);
     ZD_CHECK_LAUNCH("sort_points");
-    dfree(s.k[0], h->st); dfree(s.k[1], h->st); dfree(s.v[0], h->st); dfree(s.v[1], h->st);
+    if (!alt) { dfree(s.k[0], h->st); dfree(s.k[1], h->st); dfree(s.v[0], h->st); dfree(s.v[1], h->st); }
     dfree(s.zero_block, h->st); dfree(s.offs, h->st);
     return ZD_OK;
 }
@@ -263,7 +302,22 @@ void elapsed(zd_tree* h, int phase, int a, int b) {
 }
 
 int topology(zd_tree* h) {
-    build_topology(h->dim, h->keys, h->recs, h->n, h->leaf_max, h->tb, h->st, h->timing ? h->ev[6] : nullptr);
+    if (h->ncap < h->n - 1) {
+        // node buffers sized by count: flag + scan, read the internal-node count, grow
+        topology_flags(h->keys, h->n, h->leaf_max, h->tb, h->st);
+        ZD_CHECK_LAUNCH("topology_flags");
+        ZD_CUDA(cudaMemcpyAsync(h->h_small + 2, h->tb.block_cnt + tree_blocks(h->n), sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, h->st));
+        ZD_CUDA(cudaStreamSynchronize(h->st));
+        const int64_t nb = (int64_t)(uint32_t)h->h_small[2];
+        if (nb > h->ncap) {
+            int rc = alloc_node_bufs(h, std::min<int64_t>(h->n - 1, nb + nb / 8));
+            if (rc) return rc;
+        }
+        topology_finish(h->dim, h->keys, h->recs, h->n, h->tb, h->st, h->timing ? h->ev[6] : nullptr);
+    } else {
+        build_topology(h->dim, h->keys, h->recs, h->n, h->leaf_max, h->tb, h->st, h->timing ? h->ev[6] : nullptr);
+    }
     ZD_CHECK_LAUNCH("build_topology");
     h->host_meta_valid = false;
     return ZD_OK;
@@ -334,7 +388,7 @@ int do_build(zd_tree* h, const int32_t* points, int64_t n) {
     h->n = n;
     h->n_next = n;
     rec(h, 0);
-    if ((rc = sort_into(h, (const int32_t*)dpts, n, 0, h->keys, h->recs))) return rc;
+    if ((rc = sort_into(h, (const int32_t*)dpts, n, 0, h->keys, h->recs, true))) return rc;
     rec(h, 1);
     if ((rc = topology(h))) return rc;
     rec(h, 2);

@@ -46,6 +46,11 @@ size_t tree_blocks(int64_t n);
 // Canonical topology (K4) + bottom-up boxes (K5) over sorted keys/records.
 void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, int leaf_max,
                     const TreeBufs& t, cudaStream_t st, cudaEvent_t ev_mid);
+// The same in two halves (n >= 2): big-pair flags + block scan (the internal-node
+// count lands in block_cnt[tree_blocks(n)]), then compaction + bottom-up boxes.
+void topology_flags(const uint64_t* keys, int64_t n, int leaf_max, const TreeBufs& t, cudaStream_t st);
+void topology_finish(int dim, const uint64_t* keys, const int4* recs, int64_t n, const TreeBufs& t,
+                     cudaStream_t st, cudaEvent_t ev_mid);
 // Internal nodes in the documented zd_export layout (leaf children as ~leaf index,
 // split bit last) into out int32 [nb][4*dim+4].
 void export_nodes(int dim, const void* nodes, const int32_t* split_bit, int64_t nb, int32_t* out, cudaStream_t st);

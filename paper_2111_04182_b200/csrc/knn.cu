@@ -137,7 +137,7 @@ __device__ __forceinline__ Node<DIM> load_node(const Node<DIM>* p) {
 #ifndef ZD_UNROLL
 #define ZD_UNROLL 4
 #endif
-constexpr int kUnroll = ZD_UNROLL;   // uniform candidate loop unrolling
+[[maybe_unused]] constexpr int kUnroll = ZD_UNROLL;   // uniform candidate loop unrolling
 template <int K>
 struct Pw {
     static constexpr int v = K <= 16 ? ZD_PW : 2;   // warps per block (shared memory grows with K)

@@ -297,10 +297,28 @@ void export_nodes(int dim, const void* nodes, const int32_t* split_bit, int64_t 
 
 size_t tree_blocks(int64_t n) { return (size_t)std::max<int64_t>(1, (n - 1 + TTILE - 1) / TTILE); }
 
+void topology_flags(const uint64_t* keys, int64_t n, int leaf_max, const TreeBufs& t, cudaStream_t st) {
+    const size_t nblk = tree_blocks(n);
+    flags_kernel<<<nblk, TT, 0, st>>>(keys, (uint32_t)n, leaf_max, t.flags, t.block_cnt);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>(t.block_cnt, (uint32_t)nblk);
+    count_launch(2);
+}
+
+static void topology_boxes(int dim, const int4* recs, int64_t n, const TreeBufs& t, cudaStream_t st);
+
+void topology_finish(int dim, const uint64_t* keys, const int4* recs, int64_t n, const TreeBufs& t, cudaStream_t st,
+                     cudaEvent_t ev_mid) {
+    const int nw = dim == 2 ? (int)(sizeof(Node<2>) / 4) : (int)(sizeof(Node<3>) / 4);
+    compact_kernel<<<tree_blocks(n), TT, 0, st>>>(t.flags, keys, (uint32_t)n, t.block_cnt, t.split_bit, t.leaf_start,
+                                                  t.pt_leaf, t.d_meta, t.visit, (int32_t*)t.nodes, nw);
+    count_launch(1);
+    if (ev_mid) cudaEventRecord(ev_mid, st);
+    topology_boxes(dim, recs, n, t, st);
+}
+
 void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, int leaf_max, const TreeBufs& t,
                     cudaStream_t st, cudaEvent_t ev_mid) {
     const uint32_t un = (uint32_t)n;
-    const size_t nblk = tree_blocks(n);
     const int nw = dim == 2 ? (int)(sizeof(Node<2>) / 4) : (int)(sizeof(Node<3>) / 4);
     if (n <= 1) {
         // 0 or 1 point: a single (possibly empty) leaf; reuse the compaction kernel's
@@ -309,19 +327,17 @@ void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, 
         compact_kernel<<<1, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta, t.visit,
                                          (int32_t*)t.nodes, nw);
         count_launch(1);
+        if (ev_mid) cudaEventRecord(ev_mid, st);
+        topology_boxes(dim, recs, n, t, st);
     } else {
-        flags_kernel<<<nblk, TT, 0, st>>>(keys, un, leaf_max, t.flags, t.block_cnt);
-        scan_blocks_kernel<<<1, 1024, 0, st>>>(t.block_cnt, (uint32_t)nblk);
-        compact_kernel<<<nblk, TT, 0, st>>>(t.flags, keys, un, t.block_cnt, t.split_bit, t.leaf_start, t.pt_leaf, t.d_meta,
-                                            t.visit, (int32_t*)t.nodes, nw);
-        count_launch(3);
+        topology_flags(keys, n, leaf_max, t, st);
+        topology_finish(dim, keys, recs, n, t, st, ev_mid);
     }
-    if (ev_mid) cudaEventRecord(ev_mid, st);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // one block per BW-leaf window; leaves <= max(n, 1) (empty windows exit at once)
-    (void)sms;
+}
+
+static void topology_boxes(int dim, const int4* recs, int64_t n, const TreeBufs& t, cudaStream_t st) {
+    // one block per BW-leaf window; leaves <= max(n, 1) (windows past the last leaf exit
+    // at once, before touching the node-indexed buffers)
     int grid = (int)std::max<int64_t>(1, (std::max<int64_t>(n, 1) + BW - 1) / BW);
     count_launch(1);
     if (dim == 2)

@@ -406,3 +406,34 @@ def test_knn_warp_after_updates(zd, oracle_mod):
         gi, gd = gpu_knn_all(t, k)
         oi, od, _ = live.tree().knn_all(k)
         check_rows(gi, gd, oi, od)
+
+
+# --------------------------------------- node buffers sized from the node count
+
+@pytest.mark.parametrize("leaf_max", [1, 16])
+@pytest.mark.parametrize("dist,dim", [("uniform", 3), ("plummer", 3), ("uniform", 2), ("dup", 3)])
+def test_count_sized_node_buffers(zd, oracle_mod, monkeypatch, leaf_max, dist, dim):
+    """Above ZD_EXACT_NODES_MIN points (2^25 by default) the node-indexed tree buffers
+    are sized from each build's node count (one sync after the flag scan, growth when a
+    rebuild has more nodes).  Threshold 0 runs that path at test sizes; leaf size 1
+    forces the buffers to grow from the initial n/8 guess."""
+    monkeypatch.setenv("ZD_EXACT_NODES_MIN", "0")
+    pts = zdgen.points(dist, 9000, dim, seed=71)
+    t = zd.zd_build(dev(pts), leaf_max=leaf_max)
+    live = oracle_mod.LiveSet(pts, leaf_max=leaf_max)
+    assert_same_structure(t.zd_export(), live.tree())
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(gi, gd, oi, od)
+    b = zdgen.points(dist, 4000, dim, seed=72)
+    assert t.zd_insert(dev(b)) == live.insert(b)
+    kill = zdgen.delete_ids(9000, 3000, seed=73)
+    assert t.zd_delete(dev(kill)) == live.delete(kill)
+    assert_same_structure(t.zd_export(), live.tree())
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(gi, gd, oi, od)
+    for n in (0, 1, 2, 17):
+        small = zdgen.uniform(n, dim, seed=n)
+        ts = zd.zd_build(dev(small), leaf_max=leaf_max)
+        assert_same_structure(ts.zd_export(), oracle_mod.Tree(small, leaf_max=leaf_max))
