@@ -7,6 +7,9 @@
 activity, SIMT efficiency, stall reasons, registers, local memory traffic).
 `launches`: the `--metrics gpu__time_duration.sum` launch list, aggregated per
 kernel name: launches, total/mean ns and the share of all listed device time.
+`table`: per launch of a `--set full` capture: achieved DRAM GB/s against the
+measured HBM copy bandwidth (MEASURED_PEAKS.json), sectors per request of global
+loads/stores, issue and warp activity; JSON plus a markdown table on stdout.
 """
 from __future__ import annotations
 
@@ -99,5 +102,38 @@ def launches(path, out):
         print(f"{t['share']*100:6.2f}%  {t['launches']:4d}  {t['mean_ns']/1e3:10.1f} us  {t['kernel'][:100]}")
 
 
+def table(path, out):
+    import re
+    from pathlib import Path
+    rep(path, out)
+    d = json.load(open(out))
+    peaks = json.load(open(Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json"))
+    peak = float(peaks.get("hbm_gbs") or peaks.get("hbm_copy_gbs") or 0) or None
+    rows = []
+    for k in d["kernels"]:
+        t_ms = k["gpu__time_duration.sum"][0] * {"ms": 1, "us": 1e-3, "ns": 1e-6}.get(k["gpu__time_duration.sum"][1], 1)
+        byt = k.get("dram_bytes_per_launch", 0.0)
+        gbs = byt / (t_ms * 1e-3) / 1e9 if t_ms else 0.0
+        sec = lambda a, b: (k[a][0] / k[b][0]) if k.get(b) and k[b][0] else None  # noqa: E731
+        name = re.sub(r"\(.*", "", k["kernel"]).replace("void ", "").replace("zd::<unnamed>::", "").replace("<unnamed>::", "")
+        rows.append({"kernel": name, "grid": k.get("launch__grid_size", [None])[0], "us": round(t_ms * 1e3, 1),
+                     "dram_mb": round(byt / 1e6, 1), "gbs": round(gbs), "hbm_frac": round(gbs / peak, 3) if peak else None,
+                     "ld_sect_per_req": round(sec("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+                                                  "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum") or 0, 2),
+                     "st_sect_per_req": round(sec("l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
+                                                  "l1tex__t_requests_pipe_lsu_mem_global_op_st.sum") or 0, 2),
+                     "issue_active_pct": round(k.get("smsp__issue_active.avg.pct_of_peak_sustained_active", [0])[0], 1),
+                     "warps_active_pct": round(k.get("sm__warps_active.avg.pct_of_peak_sustained_active", [0])[0], 1),
+                     "regs": k.get("launch__registers_per_thread", [None])[0]})
+    d["table"] = rows
+    d["hbm_peak_gbs"] = peak
+    json.dump(d, open(out, "w"), indent=1)
+    print("| kernel | grid | µs | DRAM MB | GB/s | of HBM peak | ld sect/req | st sect/req | issue % | warps % |")
+    print("|---|---|---|---|---|---|---|---|---|---|")
+    for r in rows:
+        print(f"| {r['kernel']} | {r['grid']} | {r['us']} | {r['dram_mb']} | {r['gbs']} | {r['hbm_frac']} | "
+              f"{r['ld_sect_per_req']} | {r['st_sect_per_req']} | {r['issue_active_pct']} | {r['warps_active_pct']} |")
+
+
 if __name__ == "__main__":
-    {"rep": rep, "launches": launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"rep": rep, "launches": launches, "table": table}[sys.argv[1]](sys.argv[2], sys.argv[3])
