@@ -283,6 +283,7 @@ constexpr int kSortMax = 256;   // <= KW_CAP
 __device__ __forceinline__ void kw_sort(KwSh& S, int c, int lane) {
     int P = 32;
     while (P < c) P <<= 1;
+    ZD_DCHECK(P <= KW_CAP);
     for (int e = c + lane; e < P; e += 32) { S.d2[e] = INT64_MAX; S.pos[e] = INT_MAX; }
     __syncwarp();
 #pragma unroll 1
@@ -329,6 +330,7 @@ __device__ __forceinline__ void kw_scan(const int4* __restrict__ recs, int32_t s
         }
         if (hit) {
             const int slot = st.cnt + __popc(m & ((1u << lane) - 1u));
+            ZD_DCHECK(slot < KW_CAP && p >= 0);
             S.d2[slot] = d;
             S.pos[slot] = p;
         }
@@ -422,6 +424,7 @@ __global__ void __launch_bounds__(KW_WARPS * 32, ZD_KW_MINB) knn_warp_kernel(KwA
         // Alg. 3: scan the query's leaf, then ascend; at each ancestor stop if the ball
         // lies inside C's box, else search the sibling subtree
         const int32_t l = __ldg(A.qleaf + qi);
+        ZD_DCHECK(l >= 0 && l <= __ldg(A.d_meta));
         kw_scan<DIM>(A.recs, __ldg(A.leaf_start + l), __ldg(A.leaf_start + l + 1), q, S, st, A.k, lane);
         int32_t C = -1, P = __ldg(A.leaf_parent + l);
         while (P >= 0) {
