@@ -134,14 +134,23 @@ __device__ __forceinline__ Node<DIM> load_node(const Node<DIM>* p) {
 #ifndef ZD_PW
 #define ZD_PW 4
 #endif
+#ifndef ZD_PW32
+#define ZD_PW32 2         // warps per block for 16 < K <= 32
+#endif
 #ifndef ZD_UNROLL
 #define ZD_UNROLL 4
 #endif
 [[maybe_unused]] constexpr int kUnroll = ZD_UNROLL;   // uniform candidate loop unrolling
 template <int K>
 struct Pw {
-    static constexpr int v = K <= 16 ? ZD_PW : 2;   // warps per block (shared memory grows with K)
+    static constexpr int v = K <= 16 ? ZD_PW : ZD_PW32;   // warps per block (shared memory grows with K)
 };
+#ifndef ZD_MINB32
+#define ZD_MINB32 6       // 2D: min resident blocks per SM for 16 < K <= 32 (the final list spills)
+#endif
+#ifndef ZD_MINB32_3
+#define ZD_MINB32_3 8     // 3D
+#endif
 #ifndef ZD_MINB
 #define ZD_MINB 7         // 2D: min resident blocks per SM for K <= 10 (register budget)
 #endif
@@ -159,7 +168,10 @@ constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
 constexpr int kStk = ZD_STK;             // per-warp stack entries (>= tree height; 64 = key bits + 1)
 
 #ifndef ZD_MINB16
-#define ZD_MINB16 5       // min resident blocks per SM for 10 < K <= 16
+#define ZD_MINB16 5       // 2D: min resident blocks per SM for 10 < K <= 16
+#endif
+#ifndef ZD_MINB16_3
+#define ZD_MINB16_3 6     // 3D
 #endif
 #ifndef ZD_CAP_MIN
 #define ZD_CAP_MIN 22     // 2D
@@ -966,7 +978,9 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
 }
 
 template <int DIM, int K, bool EXT>
-__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? (DIM == 3 ? ZD_MINB3 : ZD_MINB) : (K <= 16 ? ZD_MINB16 : 2))) knn_packet_kernel(PacketArgs A) {
+__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? (DIM == 3 ? ZD_MINB3 : ZD_MINB)
+                                                    : (K <= 16 ? (DIM == 3 ? ZD_MINB16_3 : ZD_MINB16)
+                                                               : (DIM == 3 ? ZD_MINB32_3 : ZD_MINB32)))) knn_packet_kernel(PacketArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSh<DIM, K>* sh = reinterpret_cast<WarpSh<DIM, K>*>(smem_raw);   // Pw<K>::v warps
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
