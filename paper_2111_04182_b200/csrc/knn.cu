@@ -158,7 +158,7 @@ struct Pw {
 #define ZD_MINB3 8        // 3D (64 registers; with Cap 20 the shared memory fits 8 blocks)
 #endif
 #ifndef ZD_CH
-#define ZD_CH 16
+#define ZD_CH 32
 #endif
 constexpr int CH = ZD_CH;                // candidates tested per uniform pass
 constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
@@ -226,6 +226,12 @@ __device__ __forceinline__ Ref right_child(const Node<DIM>& nd, int32_t e) { ret
 #define ZD_PREGROUPS 1   // prefilter boxes per packet (groups of 32 / G Morton-consecutive lanes)
 #endif
 constexpr int kPG = ZD_PREGROUPS, kPGW = 32 / ZD_PREGROUPS;
+#ifndef ZD_SUB
+#define ZD_SUB 8         // 2D: candidates per unrolled sub-block of a uniform pass (divides ZD_CH)
+#endif
+#ifndef ZD_SUB3
+#define ZD_SUB3 4        // 3D
+#endif
 #ifndef ZD_FIXED_PASS
 #define ZD_FIXED_PASS 1  // uniform passes test exactly CH staged slots (masked), self excluded on hits
 #endif
@@ -481,21 +487,33 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
 #if ZD_FIXED_PASS
                 // fixed CH-wide pass (no trip-count checks); slots past cnt hold stale
                 // values and are masked off; self is excluded on the hit path
+                // in sub-blocks of ZD_SUB (uniform early exit: a short tail costs one
+                // sub-block, not a whole pass)
                 if constexpr (DIM == 3) {
                     const float wb = L.wb;
+#pragma unroll 1
+                    for (int j0 = 0; j0 < CH; j0 += ZD_SUB3) {
+                        if (j0 >= cnt) break;
 #pragma unroll
-                    for (int j = 0; j < CH; ++j) {
-                        const float4 c = S.f[h0 + j];
-                        const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
-                        const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                        if (df <= wb) hit |= 1u << j;
+                        for (int jj = 0; jj < ZD_SUB3; ++jj) {
+                            const int j = j0 + jj;
+                            const float4 c = S.f[h0 + j];
+                            const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
+                            const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                            if (df <= wb) hit |= 1u << j;
+                        }
                     }
                 } else {
                     const int64_t U = L.U;
+#pragma unroll 1
+                    for (int j0 = 0; j0 < CH; j0 += ZD_SUB) {
+                        if (j0 >= cnt) break;
 #pragma unroll
-                    for (int j = 0; j < CH; ++j) {
-                        const int4 c = S.c[h0 + j];
-                        if (dist2<DIM>(L.q, c) <= U) hit |= 1u << j;
+                        for (int jj = 0; jj < ZD_SUB; ++jj) {
+                            const int j = j0 + jj;
+                            const int4 c = S.c[h0 + j];
+                            if (dist2<DIM>(L.q, c) <= U) hit |= 1u << j;
+                        }
                     }
                 }
                 hit &= cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
