@@ -36,6 +36,7 @@
 // sound rules; the (d2, id) order makes the answer unique.  Self is excluded by id
 // (reading 13); short rows are padded with (-1, INT64_MAX) (reading 15).
 #include <climits>
+#include <cstddef>
 
 #include "common.cuh"
 #include "internal.h"
@@ -231,6 +232,9 @@ constexpr int kPG = ZD_PREGROUPS, kPGW = 32 / ZD_PREGROUPS;
 #endif
 #ifndef ZD_SUB3
 #define ZD_SUB3 4        // 3D
+#endif
+#ifndef ZD_COOP_OUT
+#define ZD_COOP_OUT 1    // stage the packet's output rows in shared memory, write them coalesced
 #endif
 #ifndef ZD_FIXED_PASS
 #define ZD_FIXED_PASS 1  // uniform passes test exactly CH staged slots (masked), self excluded on hits
@@ -981,12 +985,36 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         const int64_t d = dist2<DIM>(L.q, c);
         if (best.accepts(d, c.w)) best.insert(d, c.w);
     }
+    int32_t row = 0;
     if (active) {
-        int64_t row;
         if (EXT) row = r.w;
         else row = A.row_of_id ? __ldg(A.row_of_id + r.w) : r.w;
-        int32_t* oi = A.out_idx + row * A.k;
-        int64_t* od = A.out_d2 + row * A.k;
+    }
+    if constexpr (ZD_COOP_OUT && 12 * K <= 8 * Cap<DIM, K>::v) {
+        // cooperative row writes: the packet's rows are staged in the (now idle) buffer
+        // and written element-by-element by consecutive lanes, so one store covers ~3
+        // rows instead of 32 scattered ones
+        using WS = WarpSh<DIM, K>;
+        static_assert(offsetof(WS, bp) % 8 == 0, "int64 staging needs 8-byte alignment");
+        int64_t* sd = reinterpret_cast<int64_t*>(&S.bp[0][0]);
+        int32_t* si = reinterpret_cast<int32_t*>(sd + 32 * K);
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < K; ++t) { sd[lane * K + t] = best.d[t]; si[lane * K + t] = best.i[t]; }
+        S.p[lane] = active ? row : -1;
+        __syncwarp();
+#pragma unroll 2
+        for (int t = lane; t < 32 * K; t += 32) {
+            const int qq = t / K, ss = t - qq * K;
+            const int32_t rw = S.p[qq];
+            if (rw >= 0 && ss < A.k) {
+                A.out_idx[(int64_t)rw * A.k + ss] = si[t];
+                A.out_d2[(int64_t)rw * A.k + ss] = sd[t];
+            }
+        }
+    } else if (active) {
+        int32_t* oi = A.out_idx + (int64_t)row * A.k;
+        int64_t* od = A.out_d2 + (int64_t)row * A.k;
 #pragma unroll
         for (int s = 0; s < K; ++s) {
             if (s < A.k) { oi[s] = best.i[s]; od[s] = best.d[s]; }
