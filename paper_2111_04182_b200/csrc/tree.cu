@@ -43,35 +43,37 @@ __device__ __forceinline__ int delta_of(uint64_t a, uint64_t b) {
     return x ? 63 - __clzll((long long)x) : -1;
 }
 
-// 16-bit mask of the bytes s[p .. p+15] that are > d (signed int8, d >= 0), from
-// word loads of shared memory, funnel shifts and SIMD byte compares.
-__device__ __forceinline__ uint32_t greater_mask16(const int8_t* s, int p, int d) {
+// 16-bit mask of the bytes s[p .. p+15] that are > d, from word loads of shared
+// memory and funnel shifts.  Bytes hold delta + 1 in [0, 63] or 128 (range boundary)
+// and 1 <= d <= 63, so adding 127 - d to every byte never carries into the next one
+// and sets a byte's top bit exactly when the byte is > d: one 32-bit add per 4 bytes.
+__device__ __forceinline__ uint32_t greater_mask16(const uint8_t* s, int p, int d) {
     const int a = p & ~3, sh = (p & 3) * 8;
     const uint32_t* w = reinterpret_cast<const uint32_t*>(s + a);
     uint32_t words[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) words[i] = w[i];
-    const uint32_t dd = (uint32_t)d * 0x01010101u;
+    const uint32_t bias = (uint32_t)(127 - d) * 0x01010101u;
     uint32_t m = 0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t v = __funnelshift_r(words[i], words[i + 1], sh);
-        const uint32_t g = __vcmpgts4(v, dd) & 0x80808080u;       // 0x80 in each greater byte
-        m |= ((g * 0x00204081u) >> 28) << (4 * i);                 // byte sign bits -> 4 bits
+        const uint32_t g = (v + bias) & 0x80808080u;               // 0x80 in each greater byte
+        m |= ((g * 0x00204081u) >> 28) << (4 * i);                 // byte top bits -> 4 bits
     }
     return m;
 }
 
 __global__ void __launch_bounds__(TT) flags_kernel(const uint64_t* __restrict__ keys, uint32_t n, int leaf_max,
                                                    uint8_t* __restrict__ flags, uint32_t* __restrict__ block_cnt) {
-    __shared__ __align__(16) int8_t s_delta[TTILE + 2 * HALO + 8];
+    __shared__ __align__(16) uint8_t s_delta[TTILE + 2 * HALO + 8];   // delta + 1; 128 = boundary
     __shared__ uint32_t s_warp[32];
     const int64_t base = (int64_t)blockIdx.x * TTILE;
     const int64_t npairs = (int64_t)n - 1;
     for (int t = threadIdx.x; t < TTILE + 2 * HALO; t += TT) {
         int64_t p = base - HALO + t;
         // out-of-range pairs act as +infinity: the range boundary
-        s_delta[t] = (p >= 0 && p < npairs) ? (int8_t)delta_of(keys[p], keys[p + 1]) : (int8_t)127;
+        s_delta[t] = (p >= 0 && p < npairs) ? (uint8_t)(delta_of(keys[p], keys[p + 1]) + 1) : (uint8_t)128;
     }
     __syncthreads();
     const int W = leaf_max - 1;
@@ -82,9 +84,9 @@ __global__ void __launch_bounds__(TT) flags_kernel(const uint64_t* __restrict__ 
         const int64_t p = base + off;
         if (p >= npairs) continue;
         const int c = HALO + off;
-        const int d = s_delta[c];
+        const int d = s_delta[c];   // delta + 1
         bool big = false;
-        if (d >= 0) {
+        if (d >= 1) {
             int l = 1, r = 1;
             if (W <= 15) {
                 // branch-free: nearest larger delta within 16 bytes on each side via
