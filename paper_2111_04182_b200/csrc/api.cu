@@ -219,17 +219,22 @@ int alloc_tree_bufs(zd_tree* h, int64_t cap) {
     return alloc_node_bufs(h, cap <= exact_nodes_min() ? cap : cap / 8);
 }
 
-// Point capacity for keys/recs (and their alternates) + tree buffers.
-int ensure_point_cap(zd_tree* h, int64_t need, bool keep_primary) {
+// Point capacity for keys/recs (and their alternates) + tree buffers.  With
+// old_keys/old_recs the current primary arrays are handed back to the caller (still
+// allocated; it reads them once, e.g. as the merge source, then frees them) instead
+// of being copied into the new ones.
+int ensure_point_cap(zd_tree* h, int64_t need, uint64_t** old_keys = nullptr, int4** old_recs = nullptr) {
     if (need <= h->cap && h->keys) return ZD_OK;
     const int64_t cap = std::max<int64_t>(need, h->cap + h->cap / 4);
     uint64_t* nk = nullptr;
     int4* nr = nullptr;
     ZD_CUDA(dalloc(&nk, cap, h->st));
     ZD_CUDA(dalloc(&nr, cap, h->st));
-    if (keep_primary && h->n > 0) {
-        ZD_CUDA(cudaMemcpyAsync(nk, h->keys, h->n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, h->st));
-        ZD_CUDA(cudaMemcpyAsync(nr, h->recs, h->n * sizeof(int4), cudaMemcpyDeviceToDevice, h->st));
+    if (old_keys) {
+        *old_keys = h->keys;
+        *old_recs = h->recs;
+        h->keys = nullptr;
+        h->recs = nullptr;
     }
     dfree(h->keys, h->st); dfree(h->recs, h->st); dfree(h->keys2, h->st); dfree(h->recs2, h->st);
     dfree(h->live_ids, h->st);
@@ -383,7 +388,7 @@ int do_build(zd_tree* h, const int32_t* points, int64_t n) {
     void* owned = nullptr;
     int rc = stage_in(h, points, (size_t)n * h->dim * sizeof(int32_t), &dpts, &owned);
     if (rc) return rc;
-    if ((rc = ensure_point_cap(h, std::max<int64_t>(n, 1), false))) return rc;
+    if ((rc = ensure_point_cap(h, std::max<int64_t>(n, 1)))) return rc;
     if ((rc = ensure_id_cap(h, std::max<int64_t>(n, 1)))) return rc;
     h->n = n;
     h->n_next = n;
@@ -610,13 +615,21 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     if ((rc = sort_into(h, (const int32_t*)db, m, (uint32_t)first, bk, br))) return rc;
     if (owned) cudaFreeAsync(owned, h->st);
     rec(h, 3);
-    if ((rc = ensure_point_cap(h, h->n + m, true))) return rc;
+    // growth hands back the old primary arrays as the merge source (no copy)
+    uint64_t* src_k = h->keys;
+    int4* src_r = h->recs;
+    uint64_t* old_k = nullptr;
+    int4* old_r = nullptr;
     if ((rc = ensure_id_cap(h, first + m))) return rc;
+    if ((rc = ensure_point_cap(h, h->n + m, &old_k, &old_r))) return rc;
+    if (old_k) { src_k = old_k; src_r = old_r; }
     // merge into the alternate buffers (K8), then swap
-    merge_sorted(h->keys, h->recs, h->n, bk, br, m, h->keys2, h->recs2, h->st);
+    merge_sorted(src_k, src_r, h->n, bk, br, m, h->keys2, h->recs2, h->st);
     ZD_CHECK_LAUNCH("merge_sorted");
     std::swap(h->keys, h->keys2);
     std::swap(h->recs, h->recs2);
+    dfree(old_k, h->st);
+    dfree(old_r, h->st);
     dfree(bk, h->st);
     dfree(br, h->st);
     set_alive_range(h->alive, first, m, h->st);
