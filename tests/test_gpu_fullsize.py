@@ -51,3 +51,34 @@ def _run(zd, oracle_mod, name):
 @pytest.mark.parametrize("name", ["C2", "C3", "C4a", "C4b", "C5"])
 def test_config_full(zd, oracle_mod, name):
     _run(zd, oracle_mod, name)
+
+
+@pytest.mark.parametrize("name,k", [("C3", 100), ("C2", 100), ("C4a", 64)])
+def test_config_full_large_k(zd, oracle_mod, name, k):
+    """NEXT-3 at full size: the warp-per-query large-k kernel on a 10M-point config;
+    300 seeded sample rows vs plain brute force over all points."""
+    pts = zdgen.config_points(name)
+    t = zd.zd_build(torch.from_numpy(pts).cuda())
+    gi, gd = t.zd_knn(k)
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(99).choice(len(pts), size=300, replace=False)).astype(np.int32)
+    gi = gi[torch.from_numpy(rows).long().cuda()].cpu().numpy()
+    gd = gd[torch.from_numpy(rows).long().cuda()].cpu().numpy()
+    bi, bd = oracle_mod.brute_knn(pts, None, pts[rows], rows, k)
+    assert np.array_equal(gi, bi) and np.array_equal(gd, bd)
+    assert np.all(np.diff(gd, axis=1) >= 0)
+
+
+@pytest.mark.parametrize("name", ["C3", "C2"])
+def test_config_full_external(zd, oracle_mod, name):
+    """NEXT-1 at full size: 1M external queries (Morton-sorted and bit-located inside
+    the library) against a 10M-point tree, k = 10; 500 sample rows vs brute force."""
+    pts = zdgen.config_points(name)
+    dim = pts.shape[1]
+    q = zdgen.uniform(1_000_000, dim, seed=4242)
+    t = zd.zd_build(torch.from_numpy(pts).cuda())
+    gi, gd = t.zd_knn(K, queries=torch.from_numpy(q).cuda())
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(7).choice(len(q), size=500, replace=False))
+    bi, bd = oracle_mod.brute_knn(pts, None, q[rows], None, K)
+    assert np.array_equal(gi.cpu().numpy()[rows], bi) and np.array_equal(gd.cpu().numpy()[rows], bd)
