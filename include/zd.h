@@ -79,6 +79,16 @@ typedef struct zd_opts {
     int leaf_max;   /* leaf size bound (reading 1: leaf iff size <= leaf_max or all
                        keys equal); 0 = default 16; valid 1..ZD_LEAF_MAX_MAX */
     int timing;     /* nonzero: record per-phase device times (zd_get_timing) */
+    /* Random shift (§2, "select a random shift ... kept throughout"; Lemma 2.2
+     * P:450): shift_set != 0 adds shift[a] in [0, 2^30) to axis a of every point —
+     * build points, inserted batches and external queries alike — after the range
+     * check and before encoding.  2D only: shifted coordinates need 31 bits per axis
+     * (62-bit keys); in 3D they would need 22 bits (66-bit keys), so dim 3 with
+     * shift_set returns ZD_EINVAL.  Distances, neighbour ids and rows are unchanged
+     * (a translation); the tree is the canonical tree of the shifted points and
+     * zd_export reports shifted keys and coordinates.  The caller draws the shift. */
+    int shift_set;
+    int32_t shift[3];
 } zd_opts;
 
 /* Build a zd-tree over n points (int32 [n][dim]); point i gets id i.
@@ -154,6 +164,7 @@ typedef struct zd_info {
     int64_t n_internal;   /* internal nodes */
     int32_t root;         /* root reference: >= 0 internal node, < 0 leaf ~ref */
     int32_t node_words;   /* int32 words per exported internal node */
+    int32_t shift[3];     /* zd_opts.shift as applied (zeros: none) */
 } zd_info;
 
 ZD_API int zd_get_info(const zd_tree *h, zd_info *out);

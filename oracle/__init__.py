@@ -56,6 +56,8 @@ def lib():
         L.orc_nset_demo.argtypes = [i32, P, P, i32, P, P]
         L.orc_build.restype = P
         L.orc_build.argtypes = [P, P, i64, i32, i32]
+        L.orc_build_bits.restype = P
+        L.orc_build_bits.argtypes = [P, P, i64, i32, i32, i32]
         L.orc_free.argtypes = [P]
         L.orc_size.restype = i64
         L.orc_size.argtypes = [P]
@@ -125,13 +127,24 @@ def nset_demo(k: int, pairs):
 
 
 class Tree:
-    """Oracle zd-tree over (points, ids)."""
+    """Oracle zd-tree over (points, ids).
 
-    def __init__(self, points: np.ndarray, ids: np.ndarray | None = None, leaf_max: int = 16):
-        self.points = _c32(points)
+    shift: the random shift of P:235 ("select a random shift ... kept throughout"),
+    2D only: (sx, sy) in [0, 2^30) is added to every point (and query) and the keys
+    take 31 bits per axis.  The tree then stores the shifted coordinates."""
+
+    def __init__(self, points: np.ndarray, ids: np.ndarray | None = None, leaf_max: int = 16, shift=None):
+        pts = _c32(points)
+        self.shift = None if shift is None else np.asarray(shift, np.int64)[: pts.shape[1]]
+        if self.shift is not None:
+            if pts.shape[1] != 2:
+                raise ValueError("the random shift is 2D only (3D would need 66-bit keys)")
+            pts = _c32((pts.astype(np.int64) + self.shift).astype(np.int32))
+        self.points = pts
         self.n, self.dim = self.points.shape
         self.ids = np.arange(self.n, dtype=np.int32) if ids is None else _c32(ids)
-        self._h = lib().orc_build(_p(self.points), _p(self.ids), self.n, self.dim, leaf_max)
+        bits = (30 if self.dim == 2 else 21) + (1 if self.shift is not None else 0)
+        self._h = lib().orc_build_bits(_p(self.points), _p(self.ids), self.n, self.dim, leaf_max, bits)
         if not self._h:
             raise ValueError("orc_build failed")
         self.leaf_max = leaf_max
@@ -177,6 +190,8 @@ class Tree:
 
     def knn_queries(self, queries: np.ndarray, k: int, nthreads: int = 0, root_based: bool = False):
         q = _c32(queries)
+        if self.shift is not None:
+            q = _c32((q.astype(np.int64) + self.shift).astype(np.int32))
         m = q.shape[0]
         return self._run(lambda oi, od, c: lib().orc_knn_queries(
             self._h, _p(q), m, k, int(root_based), nthreads, _p(oi), _p(od), _p(c)), k, nthreads, m)
@@ -206,11 +221,12 @@ class LiveSet:
     returns how many were deleted (absent/dead/duplicate ids are skipped).
     """
 
-    def __init__(self, points: np.ndarray, leaf_max: int = 16):
+    def __init__(self, points: np.ndarray, leaf_max: int = 16, shift=None):
         self.points = _c32(points)
         self.ids = np.arange(self.points.shape[0], dtype=np.int32)
         self.n_next = self.points.shape[0]
         self.leaf_max = leaf_max
+        self.shift = shift
 
     def insert(self, batch: np.ndarray) -> int:
         b = _c32(batch)
@@ -227,7 +243,7 @@ class LiveSet:
         return int(kill.sum())
 
     def tree(self) -> Tree:
-        return Tree(self.points, self.ids, self.leaf_max)
+        return Tree(self.points, self.ids, self.leaf_max, shift=self.shift)
 
     def live_ids(self) -> np.ndarray:
         return np.sort(self.ids)

@@ -43,14 +43,15 @@ static int bits_per_axis(int dim) { return dim == 2 ? 30 : 21; }
 /* "taking each integer coordinate in binary form, interleaving the
  * coordinates to create one integer per point".  Level l = B-1 .. 0, axis
  * 0 .. dim-1, key = (key << 1) | bit. */
-uint64_t orc_key(const int32_t *c, int dim) {
-    int B = bits_per_axis(dim);
+static uint64_t key_bits(const int32_t *c, int dim, int B) {
     uint64_t key = 0;
     for (int l = B - 1; l >= 0; --l)
         for (int a = 0; a < dim; ++a)
             key = (key << 1) | (uint64_t)(((uint32_t)c[a] >> l) & 1u);
     return key;
 }
+
+uint64_t orc_key(const int32_t *c, int dim) { return key_bits(c, dim, bits_per_axis(dim)); }
 
 void orc_keys(const int32_t *pts, int64_t n, int dim, uint64_t *out) {
     for (int64_t i = 0; i < n; ++i) out[i] = orc_key(pts + i * dim, dim);
@@ -165,6 +166,7 @@ typedef struct orc_tree {
     int32_t nnodes, cap, root;
     int32_t *leaf_of;   /* sorted position -> leaf node */
     int64_t *row_of;    /* sorted position -> output row (rank of id among ids) */
+    int bits;          /* key bits per axis */
 } orc_tree;
 
 static int cmp_pt(const void *a, const void *b) {
@@ -235,11 +237,14 @@ static int cmp_i32(const void *a, const void *b) {
     return (x > y) - (x < y);
 }
 
-/* Build from points (row-major int32 [n][dim]) with the given ids (NULL -> 0..n-1). */
-orc_tree *orc_build(const int32_t *pts, const int32_t *ids, int64_t n, int dim, int leaf_max) {
-    if ((dim != 2 && dim != 3) || n < 0 || leaf_max < 1) return NULL;
+/* Build from points (row-major int32 [n][dim]) with the given ids (NULL -> 0..n-1),
+ * keys of `bits` bits per axis.  The random shift (§2, "select a random shift
+ * ... kept throughout") is applied by the caller to the coordinates it passes, which
+ * then need one more bit per axis (2D: 31). */
+orc_tree *orc_build_bits(const int32_t *pts, const int32_t *ids, int64_t n, int dim, int leaf_max, int bits) {
+    if ((dim != 2 && dim != 3) || n < 0 || leaf_max < 1 || bits < 1 || bits * dim > 64) return NULL;
     orc_tree *T = (orc_tree *)calloc(1, sizeof(orc_tree));
-    T->dim = dim; T->leaf_max = leaf_max; T->n = n;
+    T->dim = dim; T->leaf_max = leaf_max; T->n = n; T->bits = bits;
     T->pts = (orc_pt *)malloc(sizeof(orc_pt) * (size_t)(n ? n : 1));
     T->leaf_of = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
     T->row_of = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
@@ -247,7 +252,7 @@ orc_tree *orc_build(const int32_t *pts, const int32_t *ids, int64_t n, int dim, 
         orc_pt *p = &T->pts[i];
         p->id = ids ? ids[i] : (int32_t)i;
         p->c[0] = pts[i * dim]; p->c[1] = pts[i * dim + 1]; p->c[2] = dim == 3 ? pts[i * dim + 2] : 0;
-        p->key = orc_key(&pts[i * dim], dim);
+        p->key = key_bits(&pts[i * dim], dim, bits);
     }
     qsort(T->pts, (size_t)n, sizeof(orc_pt), cmp_pt);
     T->root = build_rec(T, 0, n, -1);
@@ -261,6 +266,10 @@ orc_tree *orc_build(const int32_t *pts, const int32_t *ids, int64_t n, int dim, 
     }
     free(sid);
     return T;
+}
+
+orc_tree *orc_build(const int32_t *pts, const int32_t *ids, int64_t n, int dim, int leaf_max) {
+    return orc_build_bits(pts, ids, n, dim, leaf_max, bits_per_axis(dim));
 }
 
 void orc_free(orc_tree *T) {
@@ -407,7 +416,7 @@ static void *run_job(void *arg) {
             Q.q = qc; Q.qid = INT32_MIN;        /* dynamic query: nothing excluded */
             row = t;
             if (T->n == 0) { /* empty tree: nothing to search */ }
-            else if (J->mode == MODE_EXT_BIT) search_up(&Q, locate_leaf(T, orc_key(qc, T->dim)));
+            else if (J->mode == MODE_EXT_BIT) search_up(&Q, locate_leaf(T, key_bits(qc, T->dim, T->bits)));
             else search_down(&Q, T->root);
         }
         write_row(&N, k, J->oi + row * k, J->od + row * k);

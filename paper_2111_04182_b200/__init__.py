@@ -38,13 +38,14 @@ class ZdError(RuntimeError):
 
 
 class _Opts(C.Structure):
-    _fields_ = [("stream", C.c_void_p), ("leaf_max", C.c_int), ("timing", C.c_int)]
+    _fields_ = [("stream", C.c_void_p), ("leaf_max", C.c_int), ("timing", C.c_int), ("shift_set", C.c_int),
+                ("shift", C.c_int32 * 3)]
 
 
 class _Info(C.Structure):
     _fields_ = [("dim", C.c_int), ("leaf_max", C.c_int), ("n", C.c_int64), ("n_next", C.c_int64),
                 ("n_leaves", C.c_int64), ("n_internal", C.c_int64), ("root", C.c_int32),
-                ("node_words", C.c_int32)]
+                ("node_words", C.c_int32), ("shift", C.c_int32 * 3)]
 
 
 def load():
@@ -216,7 +217,11 @@ class ZdTree:
     def zd_get_info(self) -> dict:
         info = _Info()
         _check(load().zd_get_info(self.handle, C.byref(info)))
-        return {f: getattr(info, f) for f, _ in _Info._fields_}
+        out = {}
+        for f, _ in _Info._fields_:
+            v = getattr(info, f)
+            out[f] = list(v) if isinstance(v, C.Array) else v
+        return out
 
     def zd_export(self) -> dict:
         """Host copies of the sorted arrays and the node arrays (numpy)."""
@@ -255,15 +260,18 @@ def zd_kernel_launches() -> int:
     return int(load().zd_kernel_launches())
 
 
-def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None, timing: bool = False) -> ZdTree:
-    """Build a zd-tree over int32 points [n, dim] (point i gets id i)."""
+def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None, timing: bool = False,
+             shift=None) -> ZdTree:
+    """Build a zd-tree over int32 points [n, dim] (point i gets id i).  shift: 2D
+    random shift (sx, sy) in [0, 2^30) applied to every point (zd_opts.shift)."""
     p = _as_i32(points)
     n = int(p.shape[0])
     dim = int(p.shape[1]) if dim is None else dim
     s = stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
     if s is None:
         s = _current_stream()
-    opts = _Opts(s, leaf_max, int(timing))
+    sh = (C.c_int32 * 3)(*(list(shift) + [0] * (3 - len(shift)))) if shift is not None else (C.c_int32 * 3)()
+    opts = _Opts(s, leaf_max, int(timing), int(shift is not None), sh)
     h = load().zd_build_ex(_ptr(p) if n else None, n, dim, C.byref(opts))
     if not h:
         raise ZdError(load().zd_last_error_code(), last_error())

@@ -137,6 +137,8 @@ struct zd_tree {
     cudaStream_t st = nullptr;
     int64_t n = 0, n_next = 0, cap = 0, id_cap = 0;
     int64_t ncap = 0;   // internal-node capacity of the node-indexed tree buffers
+    bool shift_set = false;
+    int32_t shift[3] = {0, 0, 0};   // 2D random shift, applied before encoding
     // sorted live points
     uint64_t* keys = nullptr;
     int4* recs = nullptr;
@@ -290,7 +292,7 @@ int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint
     s.zero_words = sort_zero_words(n);
     ZD_CUDA(dalloc(&s.zero_block, s.zero_words, h->st));
     ZD_CUDA(dalloc(&s.offs, 8 * 256, h->st));
-    sort_points(h->dim, dpts, n, id_base, keys_out, recs_out, s, d_invalid(h), h->st);
+    sort_points(h->dim, dpts, n, id_base, keys_out, recs_out, s, d_invalid(h), h->st, h->shift_set ? h->shift : nullptr);
     ZD_CHECK_LAUNCH("sort_points");
     if (!alt) { dfree(s.k[0], h->st); dfree(s.k[1], h->st); dfree(s.v[0], h->st); dfree(s.v[1], h->st); }
     dfree(s.zero_block, h->st); dfree(s.offs, h->st);
@@ -428,11 +430,22 @@ zd_tree* zd_build_ex(const int32_t* points, int64_t n, int dim, const zd_opts* o
     }
     const bool timing = opts && opts->timing;
     if (leaf_max < 1 || leaf_max > ZD_LEAF_MAX_MAX) { fail(ZD_EINVAL, "zd_build: leaf_max out of range"); return nullptr; }
+    const bool shift_set = opts && opts->shift_set;
+    if (shift_set) {
+        if (dim != 2) { fail(ZD_EINVAL, "zd_build: the random shift needs 66-bit keys in 3D (2D only)"); return nullptr; }
+        for (int a = 0; a < 2; ++a)
+            if (opts->shift[a] < 0 || opts->shift[a] >= (1 << 30)) { fail(ZD_EINVAL, "zd_build: shift outside [0, 2^30)"); return nullptr; }
+    }
     zd_tree* h = new zd_tree();
     h->dim = dim;
     h->leaf_max = leaf_max;
     h->st = st;
     h->timing = timing;
+    if (shift_set) {
+        h->shift_set = true;
+        h->shift[0] = opts->shift[0];
+        h->shift[1] = opts->shift[1];
+    }
     if (do_build(h, points, n) != ZD_OK) {
         std::string e = g_err;
         int c = g_err_code;
@@ -720,6 +733,7 @@ int zd_get_info(const zd_tree* hc, zd_info* out) {
     out->n_internal = h->n_internal;
     out->root = h->root;
     out->node_words = h->dim == 2 ? 12 : 16;
+    for (int a = 0; a < 3; ++a) out->shift[a] = h->shift[a];
     return ZD_OK;
 }
 

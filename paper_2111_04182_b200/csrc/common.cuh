@@ -30,7 +30,7 @@ template <> struct Dim<3> { static constexpr int B = 21; };   // 63-bit keys
 // ---- Morton interleave (§1.1; dimension 0 most significant) ----
 // Magic-number bit spreading: each coordinate's bits move to every DIM-th key bit.
 __device__ __forceinline__ uint64_t spread2(uint32_t x) {
-    uint64_t v = x & 0x3fffffffu;
+    uint64_t v = x & 0x7fffffffu;   // 30-bit coordinates, 31 with a random shift
     v = (v | (v << 16)) & 0x0000ffff0000ffffull;
     v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
     v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;

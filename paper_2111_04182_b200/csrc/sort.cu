@@ -43,24 +43,27 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
     cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(*p).store(v, cuda::memory_order_relaxed);
 }
 
+// Range check in the universe box, then the 2D random shift (zero when unset).
 template <int DIM>
-__device__ __forceinline__ uint64_t load_key_from_points(const int32_t* __restrict__ pts, uint32_t i, bool& bad) {
+__device__ __forceinline__ uint64_t load_key_from_points(const int32_t* __restrict__ pts, uint32_t i, bool& bad,
+                                                         int2 sh) {
     const int32_t* p = pts + (size_t)i * DIM;
     int x = __ldg(p), y = __ldg(p + 1), z = DIM == 3 ? __ldg(p + 2) : 0;
     bad |= !in_universe<DIM>(x, y, z);
+    if (DIM == 2) { x += sh.x; y += sh.y; }
     return morton<DIM>(x, y, z);
 }
 
 // Up-front histogram of all 8 digits (+ range validation).
 template <int DIM>
 __global__ void __launch_bounds__(256) hist_kernel(const int32_t* __restrict__ pts, uint32_t n,
-                                                   uint32_t* __restrict__ g_hist, int* __restrict__ invalid) {
+                                                   uint32_t* __restrict__ g_hist, int* __restrict__ invalid, int2 sh2) {
     __shared__ uint32_t sh[NPASS][256];
     for (int i = threadIdx.x; i < NPASS * 256; i += 256) (&sh[0][0])[i] = 0;
     __syncthreads();
     bool bad = false;
     for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
-        uint64_t key = load_key_from_points<DIM>(pts, i, bad);
+        uint64_t key = load_key_from_points<DIM>(pts, i, bad, sh2);
 #pragma unroll
         for (int p = 0; p < NPASS; ++p) atomicAdd(&sh[p][(key >> (8 * p)) & 255], 1u);
     }
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
     const int32_t* __restrict__ pts, const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ ids_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ ids_out, int4* __restrict__ recs_out,
     uint32_t n, int shift, uint32_t id_base, const uint32_t* __restrict__ digit_offs,
-    uint32_t* status, uint32_t* tile_counter) {
+    uint32_t* status, uint32_t* tile_counter, int2 psh) {
     __shared__ union {
         uint32_t hist[SW][256];
         uint64_t keys[STILE];
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
         uint32_t idx = base + j * 32;
         if (idx < n) {
             if (MODE == 0) {
-                key[j] = load_key_from_points<DIM>(pts, idx, bad);
+                key[j] = load_key_from_points<DIM>(pts, idx, bad, psh);
                 id[j] = id_base + idx;
             } else {
                 key[j] = keys_in[idx];
@@ -234,7 +237,7 @@ __global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
 
 template <int DIM>
 void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
-                   const SortScratch& s, int* d_invalid, cudaStream_t st) {
+                   const SortScratch& s, int* d_invalid, int2 psh, cudaStream_t st) {
     const uint32_t un = (uint32_t)n;
     const size_t tiles = sort_tiles(n);
     uint32_t* hist = s.zero_block;
@@ -245,7 +248,7 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int hb = (int)std::min<size_t>((size_t)sms * 8, (n + 255) / 256);
-    hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid);
+    hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid, psh);
     scan_hist_kernel<<<1, 256, 0, st>>>(hist, s.offs);
     count_launch(2 + NPASS);
     for (int p = 0; p < NPASS; ++p) {
@@ -253,13 +256,13 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
         const uint32_t* off = s.offs + p * 256;
         if (p == 0)
             onesweep_kernel<DIM, 0><<<tiles, ST, 0, st>>>(pts, nullptr, nullptr, s.k[0], s.v[0], nullptr, un, 0,
-                                                          id_base, off, stp, counters + p);
+                                                          id_base, off, stp, counters + p, psh);
         else if (p < NPASS - 1)
             onesweep_kernel<DIM, 1><<<tiles, ST, 0, st>>>(nullptr, s.k[(p - 1) & 1], s.v[(p - 1) & 1], s.k[p & 1],
-                                                          s.v[p & 1], nullptr, un, 8 * p, 0, off, stp, counters + p);
+                                                          s.v[p & 1], nullptr, un, 8 * p, 0, off, stp, counters + p, psh);
         else
             onesweep_kernel<DIM, 2><<<tiles, ST, 0, st>>>(nullptr, s.k[(p - 1) & 1], s.v[(p - 1) & 1], keys_out,
-                                                          nullptr, recs_out, un, 8 * p, 0, off, stp, counters + p);
+                                                          nullptr, recs_out, un, 8 * p, 0, off, stp, counters + p, psh);
     }
 }
 
@@ -269,10 +272,11 @@ size_t sort_tiles(int64_t n) { return (size_t)((n + STILE - 1) / STILE); }
 size_t sort_zero_words(int64_t n) { return NPASS * 256 + NPASS + (size_t)NPASS * sort_tiles(n) * 256; }
 
 void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
-                 const SortScratch& s, int* d_invalid, cudaStream_t st) {
+                 const SortScratch& s, int* d_invalid, cudaStream_t st, const int32_t* shift2) {
     if (n <= 0) return;
-    if (dim == 2) sort_points_t<2>(pts, n, id_base, keys_out, recs_out, s, d_invalid, st);
-    else sort_points_t<3>(pts, n, id_base, keys_out, recs_out, s, d_invalid, st);
+    const int2 psh = shift2 ? make_int2(shift2[0], shift2[1]) : make_int2(0, 0);
+    if (dim == 2) sort_points_t<2>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st);
+    else sort_points_t<3>(pts, n, id_base, keys_out, recs_out, s, d_invalid, make_int2(0, 0), st);
 }
 
 }  // namespace zd

@@ -437,3 +437,55 @@ def test_count_sized_node_buffers(zd, oracle_mod, monkeypatch, leaf_max, dist, d
         small = zdgen.uniform(n, dim, seed=n)
         ts = zd.zd_build(dev(small), leaf_max=leaf_max)
         assert_same_structure(ts.zd_export(), oracle_mod.Tree(small, leaf_max=leaf_max))
+
+
+# ------------------------------------------------------ random shift, 2D
+
+SHIFTS = [(0, 0), (1, 2), ((1 << 30) - 1, (1 << 30) - 1), (123456789, 987654321 % (1 << 30))]
+
+
+@pytest.mark.parametrize("shift", SHIFTS)
+@pytest.mark.parametrize("dist,leaf_max", [("uniform", 16), ("dup", 16), ("kuzmin", 16), ("uniform", 1)])
+def test_random_shift(zd, oracle_mod, dist, leaf_max, shift):
+    """zd_opts.shift: the canonical tree of the shifted points (oracle with the same
+    shift), and k-NN answers identical to the unshifted tree's (a translation)."""
+    pts = zdgen.points(dist, 12000, 2, seed=81)
+    t = zd.zd_build(dev(pts), leaf_max=leaf_max, shift=shift)
+    assert t.zd_get_info()["shift"][:2] == list(shift)
+    live = oracle_mod.LiveSet(pts, leaf_max=leaf_max, shift=shift)
+    assert_same_structure(t.zd_export(), live.tree())
+    u = zd.zd_build(dev(pts), leaf_max=leaf_max)
+    for k in (10, 50):
+        gi, gd = gpu_knn_all(t, k)
+        ui, ud = gpu_knn_all(u, k)
+        assert np.array_equal(gi, ui) and np.array_equal(gd, ud)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(*gpu_knn_all(t, 10), oi, od)
+    q = zdgen.uniform(2000, 2, seed=82)
+    qi, qd = t.zd_knn(10, queries=dev(q))
+    torch.cuda.synchronize()
+    bi, bd = oracle_mod.brute_knn(pts, None, q, None, 10)
+    check_rows(qi.cpu().numpy(), qd.cpu().numpy(), bi, bd)
+    # updates keep the shift
+    b = zdgen.points(dist, 3000, 2, seed=83)
+    assert t.zd_insert(dev(b)) == live.insert(b)
+    kill = zdgen.delete_ids(12000, 4000, seed=84)
+    assert t.zd_delete(dev(kill)) == live.delete(kill)
+    assert_same_structure(t.zd_export(), live.tree())
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(*gpu_knn_all(t, 10), oi, od)
+
+
+def test_random_shift_errors(zd):
+    with pytest.raises(zd.ZdError) as e:
+        zd.zd_build(dev(zdgen.uniform(100, 3, seed=1)), shift=(1, 2, 3))
+    assert e.value.code == zd.ZD_EINVAL
+    for bad in ((-1, 0), (0, 1 << 30)):
+        with pytest.raises(zd.ZdError) as e:
+            zd.zd_build(dev(zdgen.uniform(100, 2, seed=1)), shift=bad)
+        assert e.value.code == zd.ZD_EINVAL
+    # the range check applies to the unshifted coordinates
+    t = zd.zd_build(dev(zdgen.uniform(100, 2, seed=1)), shift=(5, 5))
+    with pytest.raises(zd.ZdError) as e:
+        t.zd_insert(dev(np.array([[1 << 30, 0]], np.int32)))
+    assert e.value.code == zd.ZD_ERANGE

@@ -361,3 +361,46 @@ def test_delete_rows_follow_live_ids(oracle_mod):
     bi, bd = oracle_mod.brute_knn(pts, ids, pts, ids, 5)
     assert np.array_equal(oi, bi) and np.array_equal(od, bd)
     check_tree_invariants(t)
+
+
+# ------------------------------------------------------------ random shift
+
+SHIFTS = [(0, 0), (1, 2), ((1 << 30) - 1, (1 << 30) - 1), (123456789, 987654321 % (1 << 30))]
+
+
+@pytest.mark.parametrize("shift", SHIFTS)
+@pytest.mark.parametrize("dist", ["uniform", "dup", "kuzmin"])
+def test_random_shift_pins(oracle_mod, dist, shift):
+    """NEXT-4 random shift (Lemma 2.2), 2D: the tree of the shifted points
+    is still a valid zd-tree (invariants), its keys are the 31-bit interleave of the
+    shifted coordinates (independent big-int bit loop), and the k-NN answer is the
+    translation-invariant plain definition: brute force on the unshifted points."""
+    pts = zdgen.points(dist, 3000, 2, seed=5)
+    t = oracle_mod.Tree(pts, shift=shift)
+    check_tree_invariants(t)
+    keys, ids, coords = t.sorted_points()
+    sp = pts.astype(np.int64) + np.asarray(shift, np.int64)
+    assert np.array_equal(coords[:, :2], sp[ids])
+    for j in range(0, len(ids), 97):
+        x, y = (int(v) for v in sp[ids[j]])
+        key = 0
+        for b in range(30, -1, -1):
+            key = (key << 2) | (((x >> b) & 1) << 1) | ((y >> b) & 1)
+        assert int(keys[j]) == key
+    rows = np.arange(len(pts), dtype=np.int32)
+    bi, bd = oracle_mod.brute_knn(pts, None, pts, rows, 10)
+    oi, od, _ = t.knn_all(10)
+    assert np.array_equal(oi, bi) and np.array_equal(od, bd)
+    q = zdgen.uniform(400, 2, seed=6)
+    qi, qd, _ = t.knn_queries(q, 7)
+    bqi, bqd = oracle_mod.brute_knn(pts, None, q, None, 7)
+    assert np.array_equal(qi, bqi) and np.array_equal(qd, bqd)
+
+
+def test_random_shift_changes_the_tree(oracle_mod):
+    # a shift that moves points across Morton cell boundaries changes the canonical tree
+    pts = zdgen.uniform(4000, 2, seed=8)
+    a, b = oracle_mod.Tree(pts), oracle_mod.Tree(pts, shift=(1 << 29, 12345))
+    assert not np.array_equal(a.sorted_points()[1], b.sorted_points()[1])
+    with pytest.raises(ValueError):
+        oracle_mod.Tree(zdgen.uniform(10, 3, seed=1), shift=(1, 2, 3))
