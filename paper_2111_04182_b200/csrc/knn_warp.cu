@@ -32,7 +32,7 @@ constexpr int KW_CAP = 2 * 128 + 64;   // buffered candidates per query (>= ZD_K
 constexpr int KW_WARPS = 4;            // warps (queries) per block
 constexpr int KW_STK = kMaxDepth;      // DFS stack: at most one far child per tree level
 #ifndef ZD_KW_COARSE
-#define ZD_KW_COARSE 32                // subtrees of <= this many points are scanned as one span
+#define ZD_KW_COARSE 128               // subtrees of <= this many points are scanned as one span (32-wide chunks)
 #endif
 #ifndef ZD_KW_MINB
 #define ZD_KW_MINB 8
