@@ -250,8 +250,7 @@ struct WarpSh {
 #endif
     int32_t p[32];                       // their sorted positions
     float4 pb[2 * kPG];                  // query box of each lane group (lo, hi; 2D: int bits)
-    int32_t bp[Cap<DIM, K>::v][32];           // per-lane buffered positions; column = lane
-    float bf[Cap<DIM, K>::v][32];             //   ... and their d2 rounded up to fp32
+    int2 be[Cap<DIM, K>::v][32];              // per-lane buffer (position, fp32 bits of ru(d2)); column = lane
     int4 stk[kStk];                      // (ref, s, e, parent | side << 31): box reloaded on pop
 #ifdef ZD_DEBUG
     int32_t dbg_npts, dbg_nint;          // bounds for ZD_DCHECK
@@ -349,10 +348,9 @@ __device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<DIM, K>& S, int 
     const float F = DIM == 3 ? __fmul_ru(L.fa[K - 1], 1.0f + 0x1p-20f) : L.fa[K - 1];
     int w = 0;
     for (int e = 0; e < L.cnt; ++e) {
-        const float f = S.bf[e][lane];
-        const int32_t p = S.bp[e][lane];
-        S.bf[w][lane] = f;
-        S.bp[w][lane] = p;
+        const int2 v = S.be[e][lane];
+        const float f = __int_as_float(v.y);
+        S.be[w][lane] = v;
         w += (f <= F) ? 1 : 0;
     }
     L.cnt = w;
@@ -366,15 +364,15 @@ template <int DIM, int K>
 __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Query<DIM> q, int cnt, WarpSh<DIM, K>& S,
                                                int lane) {
     for (int e = 0; e < cnt; ++e) {
-        const int4 ce = __ldg(recs + S.bp[e][lane]);
+        const int4 ce = __ldg(recs + S.be[e][lane].x);
         const int64_t de = dist2<DIM>(q, ce);
         int rank = 0;
         for (int f = 0; f < cnt; ++f) {
-            const int4 cf = __ldg(recs + S.bp[f][lane]);
+            const int4 cf = __ldg(recs + S.be[f][lane].x);
             const int64_t dv = dist2<DIM>(q, cf);
             rank += (dv < de || (dv == de && cf.w < ce.w)) ? 1 : 0;
         }
-        if (rank >= K) S.bf[e][lane] = INFINITY;
+        if (rank >= K) S.be[e][lane].y = __float_as_int(INFINITY);
     }
 }
 
@@ -622,8 +620,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                     }
                 }
                 ZD_DCHECK((L.cnt < Cap<DIM, K>::v));
-                S.bp[L.cnt][lane] = S.p[j];
-                S.bf[L.cnt][lane] = xf;
+                S.be[L.cnt][lane] = make_int2(S.p[j], __float_as_int(xf));
                 ++L.cnt;
             }
         }
@@ -981,7 +978,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
     KBest<K> best;
     best.init();
     for (int e = 0; e < L.cnt; ++e) {
-        const int4 c = __ldg(A.recs + S.bp[e][lane]);
+        const int4 c = __ldg(A.recs + S.be[e][lane].x);
         const int64_t d = dist2<DIM>(L.q, c);
         if (best.accepts(d, c.w)) best.insert(d, c.w);
     }
@@ -995,8 +992,8 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         // and written element-by-element by consecutive lanes, so one store covers ~3
         // rows instead of 32 scattered ones
         using WS = WarpSh<DIM, K>;
-        static_assert(offsetof(WS, bp) % 8 == 0, "int64 staging needs 8-byte alignment");
-        int64_t* sd = reinterpret_cast<int64_t*>(&S.bp[0][0]);
+        static_assert(offsetof(WS, be) % 8 == 0, "int64 staging needs 8-byte alignment");
+        int64_t* sd = reinterpret_cast<int64_t*>(&S.be[0][0]);
         int32_t* si = reinterpret_cast<int32_t*>(sd + 32 * K);
         __syncwarp();
 #pragma unroll
