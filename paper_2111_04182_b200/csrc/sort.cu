@@ -57,13 +57,15 @@ __device__ __forceinline__ uint64_t load_key_from_points(const int32_t* __restri
 // Up-front histogram of all 8 digits (+ range validation).
 template <int DIM>
 __global__ void __launch_bounds__(256) hist_kernel(const int32_t* __restrict__ pts, uint32_t n,
-                                                   uint32_t* __restrict__ g_hist, int* __restrict__ invalid, int2 sh2) {
+                                                   uint32_t* __restrict__ g_hist, int* __restrict__ invalid, int2 sh2,
+                                                   uint64_t* __restrict__ keys_out) {
     __shared__ uint32_t sh[NPASS][256];
     for (int i = threadIdx.x; i < NPASS * 256; i += 256) (&sh[0][0])[i] = 0;
     __syncthreads();
     bool bad = false;
     for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
         uint64_t key = load_key_from_points<DIM>(pts, i, bad, sh2);
+        keys_out[i] = key;   // the first pass reads these instead of re-encoding
 #pragma unroll
         for (int p = 0; p < NPASS; ++p) atomicAdd(&sh[p][(key >> (8 * p)) & 255], 1u);
     }
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
         uint32_t idx = base + j * 32;
         if (idx < n) {
             if (MODE == 0) {
-                key[j] = load_key_from_points<DIM>(pts, idx, bad, psh);
+                key[j] = keys_in[idx];   // encoded (and range-checked) by hist_kernel
                 id[j] = id_base + idx;
             } else {
                 key[j] = keys_in[idx];
@@ -248,14 +250,14 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int hb = (int)std::min<size_t>((size_t)sms * 8, (n + 255) / 256);
-    hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid, psh);
+    hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid, psh, s.k[1]);
     scan_hist_kernel<<<1, 256, 0, st>>>(hist, s.offs);
     count_launch(2 + NPASS);
     for (int p = 0; p < NPASS; ++p) {
         uint32_t* stp = status + (size_t)p * tiles * 256;
         const uint32_t* off = s.offs + p * 256;
         if (p == 0)
-            onesweep_kernel<DIM, 0><<<tiles, ST, 0, st>>>(pts, nullptr, nullptr, s.k[0], s.v[0], nullptr, un, 0,
+            onesweep_kernel<DIM, 0><<<tiles, ST, 0, st>>>(pts, s.k[1], nullptr, s.k[0], s.v[0], nullptr, un, 0,
                                                           id_base, off, stp, counters + p, psh);
         else if (p < NPASS - 1)
             onesweep_kernel<DIM, 1><<<tiles, ST, 0, st>>>(nullptr, s.k[(p - 1) & 1], s.v[(p - 1) & 1], s.k[p & 1],
