@@ -65,6 +65,20 @@ __global__ void k_imad_wide(long long* out, int b, int c) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void k_imnmx(int* out, int b, int c) {
+    int a[CH];
+    for (int i = 0; i < CH; ++i) a[i] = threadIdx.x + i;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            asm volatile("max.s32 %0, %0, %1;" : "+r"(a[i]) : "r"(b));
+            asm volatile("min.s32 %0, %0, %1;" : "+r"(a[i]) : "r"(c));
+        }
+    int s = 0;
+    for (int i = 0; i < CH; ++i) s += a[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 // 64-bit compare + select (setp.lt.s64 + selp.b64): the candidate test of the 2D path
 __global__ void k_cmp64(long long* out, long long b, long long c) {
     long long a[CH];
@@ -107,10 +121,11 @@ int main() {
     void* buf = nullptr;
     cudaMalloc(&buf, (size_t)blocks * threads * 8);
     const double per = (double)ITERS * CH;
-    struct R { const char* name; double ops; } res[6];
+    struct R { const char* name; double ops; } res[8];
     int nr = 0;
     res[nr++] = {"FFMA", run([&] { k_ffma<<<blocks, threads>>>((float*)buf, 1.0001f, 0.5f); }, blocks, threads, per)};
     res[nr++] = {"FMNMX", run([&] { k_fmnmx<<<blocks, threads>>>((float*)buf, 1.0f, 2.0f); }, blocks, threads, 2 * per)};
+    res[nr++] = {"IMNMX", run([&] { k_imnmx<<<blocks, threads>>>((int*)buf, 3, 1 << 20); }, blocks, threads, 2 * per)};
     res[nr++] = {"IADD", run([&] { k_iadd3<<<blocks, threads>>>((int*)buf, 3, 5); }, blocks, threads, 2 * per)};
     res[nr++] = {"IMAD.WIDE", run([&] { k_imad_wide<<<blocks, threads>>>((long long*)buf, 3, 5); }, blocks, threads, per)};
     res[nr++] = {"ISETP64+SEL", run([&] { k_cmp64<<<blocks, threads>>>((long long*)buf, 1000, 7); }, blocks, threads, per)};
