@@ -187,13 +187,31 @@ __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ 
     }
     __syncthreads();
     {
+        // node b0+t (= s_sb[t+1]) is window-local iff a larger split bit exists in
+        // s_sb[0..t] and in s_sb[t+2..BW]: a block prefix-max and suffix-max scan
+        __shared__ int32_t s_wmax[2][BW / 32];
+        __shared__ int32_t s_suf[BW];
+        const int lane = t & 31, wi = t >> 5;
+        int32_t pv = s_sb[t], sv = s_sb[t + 1];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, pv, o);
+            const int32_t z = __shfl_down_sync(0xffffffffu, sv, o);
+            if (lane >= o) pv = max(pv, y);
+            if (lane + o < 32) sv = max(sv, z);
+        }
+        if (lane == 31) s_wmax[0][wi] = pv;
+        if (lane == 0) s_wmax[1][wi] = sv;
+        __syncthreads();
+        for (int w = 0; w < wi; ++w) pv = max(pv, s_wmax[0][w]);              // max s_sb[0..t]
+        for (int w = wi + 1; w < BW / 32; ++w) sv = max(sv, s_wmax[1][w]);     // max s_sb[t+1..BW]
+        s_suf[t] = sv;
+        __syncthreads();
         bool loc = false;
-        if (b0 + t < nb) {   // node b0+t = s_sb[t+1]
+        if (b0 + t < nb) {
             const int32_t d = s_sb[t + 1];
-            bool lok = false, rok = false;
-            for (int i = t; i >= 0; --i) if (s_sb[i] > d) { lok = true; break; }
-            for (int i = t + 2; i <= BW; ++i) if (s_sb[i] > d) { rok = true; break; }
-            loc = lok && rok;
+            const int32_t rmax = t + 1 < BW ? s_suf[t + 1] : INT32_MIN;     // max s_sb[t+2..BW]
+            loc = pv > d && rmax > d;
         }
         s_local[t] = loc;
         s_visit[t] = 0u;
