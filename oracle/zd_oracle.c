@@ -13,6 +13,8 @@
  * What it computes:
  *   keys   — Morton interleave by a scalar bit loop (§1.1; S:49 dim 0 most
  *            significant within a bit group).  Deliberately NOT a magic-number spread.
+ *            B = 30 (2D) / 21 (3D) bits per axis; 31 in 2D when the caller applies
+ *            the random shift of P:235 (orc_build_bits; the Python Tree(shift=)).
  *   sort   — qsort by (key, id) (§2).
  *   build  — recursive Alg. 1 buildTree/splitUsingBit with empty
  *            cuts skipped: leaf iff size <= leaf_max or all keys equal
