@@ -164,6 +164,10 @@ __device__ __forceinline__ void store_box(typename BoxT<DIM>::T* dst, const int3
 // (the canonical tree is the Cartesian tree of the split bits), found by scanning the
 // window's split bits in shared memory.
 constexpr int BW = 128;
+#ifndef ZD_LEAF_UNROLL
+#define ZD_LEAF_UNROLL 4
+#endif
+constexpr int kLeafUnroll = ZD_LEAF_UNROLL;   // leaf-box record loads in flight per thread
 
 template <int DIM>
 __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ recs, const int32_t* __restrict__ leaf_start,
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ 
 #pragma unroll
         for (int a = 0; a < DIM; ++a) { bb[a] = INT32_MAX; bb[DIM + a] = INT32_MIN; }
         const int32_t s = s_ls[t], e = lstart(l + 1);
-#pragma unroll 4
+#pragma unroll kLeafUnroll
         for (int32_t j = s; j < e; ++j) {
             const int4 r = __ldg(recs + j);
             const int c[3] = {r.x, r.y, r.z};
