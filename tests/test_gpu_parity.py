@@ -489,3 +489,61 @@ def test_random_shift_errors(zd):
     with pytest.raises(zd.ZdError) as e:
         t.zd_insert(dev(np.array([[1 << 30, 0]], np.int32)))
     assert e.value.code == zd.ZD_ERANGE
+
+
+# ------------------------------------------------------------- adversarial inputs
+
+def _adversarial(kind, dim):
+    B = 30 if dim == 2 else 21
+    top = (1 << B) - 1
+    rng = np.random.default_rng(17)
+    if kind == "deep":
+        # one point per power of two on every axis: each split peels off one point, so
+        # with leaf size 1 the canonical tree reaches depth ~dim*B (the 64-level bound)
+        pts = [np.zeros(dim, np.int64)]
+        for a in range(dim):
+            for j in range(B):
+                p = np.zeros(dim, np.int64)
+                p[a] = 1 << j
+                pts.append(p)
+                q = np.full(dim, top, np.int64)
+                q[a] = top - (1 << j)
+                pts.append(q)
+        return np.array(pts, np.int32)
+    if kind == "collinear":
+        x = rng.integers(0, 1 << B, size=4000)
+        return np.stack([x] + [np.full(4000, 12345)] * (dim - 1), axis=1).astype(np.int32)
+    if kind == "two_corners":
+        a = rng.integers(0, 64, size=(3000, dim))
+        return np.concatenate([a, top - a]).astype(np.int32)
+    if kind == "one_site_plus_outliers":
+        a = np.full((3000, dim), 777)
+        b = rng.integers(0, 1 << B, size=(20, dim))
+        return np.concatenate([a, b]).astype(np.int32)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["deep", "collinear", "two_corners", "one_site_plus_outliers"])
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("leaf_max", [1, 16])
+def test_adversarial_inputs(zd, oracle_mod, kind, dim, leaf_max):
+    pts = _adversarial(kind, dim)
+    t = zd.zd_build(dev(pts), leaf_max=leaf_max)
+    assert_same_structure(t.zd_export(), oracle_mod.Tree(pts, leaf_max=leaf_max))
+    rows = np.arange(len(pts), dtype=np.int32)
+    for k, warp in ((1, False), (10, False), (10, True), (100, False)):
+        gi, gd = t.zd_knn(k, warp=warp)
+        torch.cuda.synchronize()
+        bi, bd = oracle_mod.brute_knn(pts, None, pts, rows, k)
+        check_rows(gi.cpu().numpy(), gd.cpu().numpy(), bi, bd)
+    q = _adversarial(kind, dim)[::3]
+    gi, gd = t.zd_knn(10, queries=dev(q))
+    torch.cuda.synchronize()
+    bi, bd = oracle_mod.brute_knn(pts, None, q, None, 10)
+    check_rows(gi.cpu().numpy(), gd.cpu().numpy(), bi, bd)
+    if dim == 2:
+        s = zd.zd_build(dev(pts), leaf_max=leaf_max, shift=(1 << 29, 3))
+        gi, gd = s.zd_knn(10)
+        torch.cuda.synchronize()
+        bi, bd = oracle_mod.brute_knn(pts, None, pts, rows, 10)
+        check_rows(gi.cpu().numpy(), gd.cpu().numpy(), bi, bd)
