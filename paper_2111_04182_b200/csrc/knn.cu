@@ -475,8 +475,14 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
 #endif
         }
         __syncwarp();
+#if ZD_CH >= 32
+        {   // one pass covers the whole staged chunk (n32 <= 32)
+            constexpr int h0 = 0;
+            const int cnt = n32;
+#else
         for (int h0 = 0; h0 < n32; h0 += CH) {
             const int cnt = min(CH, n32 - h0);
+#endif
             // compact (all lanes together) once some needing lane is nearly full; a lane
             // that still fills up while taking hits compacts on its own (take_hit)
             if (__any_sync(0xffffffffu, need && L.cnt > Cap<DIM, K>::v - ZD_SLACK)) {
