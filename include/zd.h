@@ -165,6 +165,9 @@ typedef struct zd_info {
     int32_t root;         /* root reference: >= 0 internal node, < 0 leaf ~ref */
     int32_t node_words;   /* int32 words per exported internal node */
     int32_t shift[3];     /* zd_opts.shift as applied (zeros: none) */
+    int64_t fast_inserts; /* inserts applied without a topology rebuild (NEXT-2 fast
+                             path: the batch kept the canonical topology; ZD_INCR=0
+                             in the environment disables it) */
 } zd_info;
 
 ZD_API int zd_get_info(const zd_tree *h, zd_info *out);

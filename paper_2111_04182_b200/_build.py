@@ -11,7 +11,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_PATH = PKG / "libzd.so"
 STATS_LIB_PATH = PKG / "libzd_stats.so"   # profiling variant (-DZD_KNN_STATS work counters)
-SOURCES = ["sort.cu", "tree.cu", "knn.cu", "knn_warp.cu", "update.cu", "api.cu"]
+SOURCES = ["sort.cu", "tree.cu", "knn.cu", "knn_warp.cu", "update.cu", "incr.cu", "api.cu"]
 DEPS = SOURCES + ["common.cuh", "internal.h"]
 
 NVCC_FLAGS = [

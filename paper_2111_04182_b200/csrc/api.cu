@@ -137,6 +137,7 @@ struct zd_tree {
     cudaStream_t st = nullptr;
     int64_t n = 0, n_next = 0, cap = 0, id_cap = 0;
     int64_t ncap = 0;   // internal-node capacity of the node-indexed tree buffers
+    int64_t fast_inserts = 0;   // inserts applied by the NEXT-2 fast path (introspection/tests)
     bool shift_set = false;
     int32_t shift[3] = {0, 0, 0};   // 2D random shift, applied before encoding
     // sorted live points
@@ -225,7 +226,8 @@ int alloc_tree_bufs(zd_tree* h, int64_t cap) {
 // old_keys/old_recs the current primary arrays are handed back to the caller (still
 // allocated; it reads them once, e.g. as the merge source, then frees them) instead
 // of being copied into the new ones.
-int ensure_point_cap(zd_tree* h, int64_t need, uint64_t** old_keys = nullptr, int4** old_recs = nullptr) {
+int ensure_point_cap(zd_tree* h, int64_t need, uint64_t** old_keys = nullptr, int4** old_recs = nullptr,
+                     bool keep_nodes = false) {
     if (need <= h->cap && h->keys) return ZD_OK;
     const int64_t cap = std::max<int64_t>(need, h->cap + h->cap / 4);
     uint64_t* nk = nullptr;
@@ -247,6 +249,16 @@ int ensure_point_cap(zd_tree* h, int64_t need, uint64_t** old_keys = nullptr, in
     ZD_CUDA(dalloc(&h->live_ids, cap, h->st));
     h->cap = cap;
     h->rows_dirty = true;   // live_ids was reallocated
+    if (keep_nodes && h->tb.nodes) {
+        // the insert fast path keeps the node-indexed buffers: only the point-indexed
+        // ones grow (their contents are rewritten by the fast path)
+        TreeBufs& t = h->tb;
+        dfree(t.pt_leaf, h->st); dfree(t.flags, h->st); dfree(t.block_cnt, h->st);
+        ZD_CUDA(dalloc(&t.pt_leaf, cap, h->st));
+        ZD_CUDA(dalloc(&t.flags, cap, h->st));
+        ZD_CUDA(dalloc(&t.block_cnt, std::max(tree_blocks(cap), compact_blocks(cap)) + 2, h->st));
+        return ZD_OK;
+    }
     return alloc_tree_bufs(h, cap);
 }
 
@@ -306,6 +318,13 @@ void rec(zd_tree* h, int i) {
 void elapsed(zd_tree* h, int phase, int a, int b) {
     float t = 0.f;
     if (h->timing && cudaEventElapsedTime(&t, h->ev[a], h->ev[b]) == cudaSuccess) h->ms[phase] = t;
+}
+
+// NEXT-2 insert fast path: batches up to this size are checked; ZD_INCR=0 disables it.
+constexpr int64_t kIncrMaxBatch = (int64_t)1 << 16;
+bool incr_enabled() {
+    const char* e = std::getenv("ZD_INCR");
+    return !(e && e[0] == '0');
 }
 
 int topology(zd_tree* h) {
@@ -607,17 +626,12 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     const void* db = nullptr;
     void* owned = nullptr;
     if ((rc = stage_in(h, batch, (size_t)m * h->dim * sizeof(int32_t), &db, &owned))) return rc;
-    // validation before any mutation
+    // validation before any mutation.  The batch is sorted first (it only
+    // writes scratch) so that the fast-path check below shares the one sync.
     rec(h, 0);
-    ZD_CUDA(cudaMemsetAsync(d_invalid(h), 0, sizeof(int), h->st));
+    ZD_CUDA(cudaMemsetAsync(d_invalid(h), 0, 2 * sizeof(int), h->st));   // [4] invalid, [5] fast path refused
     validate_points(h->dim, (const int32_t*)db, m, d_invalid(h), h->st);
-    ZD_CUDA(cudaMemcpyAsync(h->h_small + 4, d_invalid(h), sizeof(int), cudaMemcpyDeviceToHost, h->st));
     rec(h, 1);
-    ZD_CUDA(cudaStreamSynchronize(h->st));
-    if (h->h_small[4]) {
-        if (owned) cudaFreeAsync(owned, h->st);
-        return fail(ZD_ERANGE, "zd_insert: coordinate outside the universe box (tree unchanged)");
-    }
     const int64_t first = h->n_next;
     // sorted batch with ids first.. (K7)
     uint64_t* bk = nullptr;
@@ -627,6 +641,24 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     rec(h, 2);
     if ((rc = sort_into(h, (const int32_t*)db, m, (uint32_t)first, bk, br))) return rc;
     if (owned) cudaFreeAsync(owned, h->st);
+    // NEXT-2 fast path (incr.cu): a batch that keeps the canonical topology is applied
+    // by position shifts and a box refit instead of the full rebuild
+    int32_t* bleaf = nullptr;
+    const bool try_fast = incr_enabled() && h->n > 1 && m <= kIncrMaxBatch;
+    if (try_fast) {
+        ZD_CUDA(dalloc(&bleaf, m, h->st));
+        KnnArgs t{};
+        t.nodes = h->tb.nodes; t.split_bit = h->tb.split_bit; t.d_meta = h->d_small; t.leaf_start = h->tb.leaf_start;
+        incr_locate(h->dim, bk, m, t, h->keys, h->leaf_max, bleaf, d_invalid(h) + 1, h->st);
+        ZD_CHECK_LAUNCH("incr_locate");
+    }
+    ZD_CUDA(cudaMemcpyAsync(h->h_small + 4, d_invalid(h), 2 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    ZD_CUDA(cudaStreamSynchronize(h->st));
+    if (h->h_small[4]) {
+        dfree(bk, h->st); dfree(br, h->st); dfree(bleaf, h->st);
+        return fail(ZD_ERANGE, "zd_insert: coordinate outside the universe box (tree unchanged)");
+    }
+    const bool fast = try_fast && !h->h_small[5];
     rec(h, 3);
     // growth hands back the old primary arrays as the merge source (no copy)
     uint64_t* src_k = h->keys;
@@ -634,7 +666,7 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     uint64_t* old_k = nullptr;
     int4* old_r = nullptr;
     if ((rc = ensure_id_cap(h, first + m))) return rc;
-    if ((rc = ensure_point_cap(h, h->n + m, &old_k, &old_r))) return rc;
+    if ((rc = ensure_point_cap(h, h->n + m, &old_k, &old_r, fast))) return rc;
     if (old_k) { src_k = old_k; src_r = old_r; }
     // merge into the alternate buffers (K8), then swap
     merge_sorted(src_k, src_r, h->n, bk, br, m, h->keys2, h->recs2, h->st);
@@ -643,14 +675,26 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     std::swap(h->recs, h->recs2);
     dfree(old_k, h->st);
     dfree(old_r, h->st);
+    if (fast) {
+        if ((rc = refresh_host_meta(h))) return rc;   // no-op when valid (it is after a build)
+        incr_apply(h->dim, h->n_internal, bleaf, br, m, h->tb.leaf_start, h->tb.pt_leaf, h->tb.nodes, h->tb.range,
+                   h->tb.pos_range, h->tb.leaf_parent, h->st);
+        ZD_CHECK_LAUNCH("incr_apply");
+        h->fast_inserts += 1;
+    }
     dfree(bk, h->st);
     dfree(br, h->st);
+    dfree(bleaf, h->st);
     set_alive_range(h->alive, first, m, h->st);
     h->n += m;
     h->n_next += m;
     if (!h->rows_identity) h->rows_dirty = true;
     rec(h, 4);
-    if ((rc = topology(h))) return rc;
+    if (fast) {
+        if (h->timing) ZD_CUDA(cudaEventRecord(h->ev[6], h->st));   // no topology / box phase
+    } else if ((rc = topology(h))) {
+        return rc;
+    }
     rec(h, 5);
     if (h->timing) {
         ZD_CUDA(cudaEventSynchronize(h->ev[5]));
@@ -734,6 +778,7 @@ int zd_get_info(const zd_tree* hc, zd_info* out) {
     out->root = h->root;
     out->node_words = h->dim == 2 ? 12 : 16;
     for (int a = 0; a < 3; ++a) out->shift[a] = h->shift[a];
+    out->fast_inserts = h->fast_inserts;
     return ZD_OK;
 }
 

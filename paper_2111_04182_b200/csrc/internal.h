@@ -83,6 +83,14 @@ struct KnnArgs {
 constexpr int kPacketKMax = 32;   // largest k of the packet kernel; above: knn_warp
 // Large-k path (knn_warp.cu): one warp per query over Morton-ordered queries.
 void knn_warp(const KnnArgs& a, const int4* qrecs, const int32_t* qleaf, int64_t nq, bool ext, cudaStream_t st);
+// NEXT-2 insert fast path (incr.cu): leaf of each sorted batch key by its bits, *bad set
+// if a key leaves its leaf's cell or a leaf would exceed leaf_max; then the in-place
+// position shifts and box refit for a batch that keeps the topology.
+void incr_locate(int dim, const uint64_t* bkeys, int64_t m, const KnnArgs& t, const uint64_t* keys, int leaf_max,
+                 int32_t* bleaf, int* bad, cudaStream_t st);
+void incr_apply(int dim, int64_t nb, const int32_t* bleaf, const int4* brecs, int64_t m, int32_t* leaf_start,
+                int32_t* pt_leaf, void* nodes, const int32_t* range, int2* pos_range, const int32_t* leaf_parent,
+                cudaStream_t st);
 // Work counters of the packet k-NN kernel (only in a -DZD_KNN_STATS build).
 enum { ZS_PACKETS = 0, ZS_QUERIES, ZS_NODES, ZS_POPS, ZS_ASCENTS, ZS_SPANS, ZS_PASSES, ZS_CAND, ZS_HITS,
        ZS_ROUNDS, ZS_COMPACT, ZS_SURV, ZS_SURV_MAX, ZS_CYCLES, ZS_MAXPKT, ZS_DEFERRED, ZS_HIST0, ZD_NSTATS = ZS_HIST0 + 32 };

@@ -547,3 +547,82 @@ def test_adversarial_inputs(zd, oracle_mod, kind, dim, leaf_max):
         torch.cuda.synchronize()
         bi, bd = oracle_mod.brute_knn(pts, None, pts, rows, 10)
         check_rows(gi.cpu().numpy(), gd.cpu().numpy(), bi, bd)
+
+
+# ------------------------------------------- NEXT-2: insert fast path (incr.cu)
+
+def _fitting_batch(t, pts, per_leaf, perturb, seed):
+    """Points placed in leaves with spare room: copies of a leaf's point, optionally
+    with the lowest coordinate bit flipped (stays in the leaf's Morton cell)."""
+    ex = t.zd_export()
+    ls = ex["leaf_start"]
+    sizes = np.diff(ls)
+    rng = np.random.default_rng(seed)
+    leaves = np.nonzero(sizes <= 16 - per_leaf)[0]
+    leaves = rng.choice(leaves, size=min(len(leaves), 300), replace=False)
+    out = []
+    for l in leaves:
+        rec = ex["recs"][ls[l]]
+        for _ in range(per_leaf):
+            p = rec[:pts.shape[1]].astype(np.int64).copy()
+            if perturb:
+                p[rng.integers(0, pts.shape[1])] ^= 1
+            out.append(p)
+    return np.array(out, np.int32)
+
+
+@pytest.mark.parametrize("dist,dim", [("uniform", 3), ("plummer", 3), ("uniform", 2), ("kuzmin", 2)])
+@pytest.mark.parametrize("perturb", [False, True])
+def test_insert_fast_path(zd, oracle_mod, monkeypatch, dist, dim, perturb):
+    monkeypatch.delenv("ZD_INCR", raising=False)
+    pts = zdgen.points(dist, 40000, dim, seed=91)
+    t = zd.zd_build(dev(pts))
+    live = oracle_mod.LiveSet(pts)
+    fast0 = t.zd_get_info()["fast_inserts"]
+    for r in range(3):   # first insert grows the capacity, later ones do not
+        b = _fitting_batch(t, pts, 1 + r % 2, perturb, seed=r)
+        assert t.zd_insert(dev(b)) == live.insert(b)
+        assert_same_structure(t.zd_export(), live.tree())
+    info = t.zd_get_info()
+    assert info["fast_inserts"] - fast0 >= 2, "the fitting batches should take the fast path"
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(gi, gd, oi, od)
+    # a random batch overflows leaves: full rebuild, still canonical
+    b = zdgen.points(dist, 3000, dim, seed=95)
+    before = t.zd_get_info()["fast_inserts"]
+    assert t.zd_insert(dev(b)) == live.insert(b)
+    assert t.zd_get_info()["fast_inserts"] == before
+    assert_same_structure(t.zd_export(), live.tree())
+    # after a delete (topology rebuilt) the fast path applies again
+    kill = zdgen.delete_ids(40000, 500, seed=96)
+    assert t.zd_delete(dev(kill)) == live.delete(kill)
+    b = _fitting_batch(t, pts, 1, perturb, seed=97)
+    assert t.zd_insert(dev(b)) == live.insert(b)
+    assert_same_structure(t.zd_export(), live.tree())
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(gi, gd, oi, od)
+    q = zdgen.uniform(1000, dim, seed=98)
+    qi, qd = t.zd_knn(16, queries=dev(q))
+    torch.cuda.synchronize()
+    oqi, oqd, _ = live.tree().knn_queries(q, 16)
+    check_rows(qi.cpu().numpy(), qd.cpu().numpy(), oqi, oqd)
+
+
+def test_insert_fast_path_disabled_and_shifted(zd, oracle_mod, monkeypatch):
+    pts = zdgen.uniform(30000, 2, seed=92)
+    monkeypatch.setenv("ZD_INCR", "0")
+    t = zd.zd_build(dev(pts))
+    b = _fitting_batch(t, pts, 1, True, seed=1)
+    t.zd_insert(dev(b))
+    assert t.zd_get_info()["fast_inserts"] == 0
+    monkeypatch.delenv("ZD_INCR")
+    s = zd.zd_build(dev(pts), shift=(123457, 1 << 29))
+    live = oracle_mod.LiveSet(pts, shift=(123457, 1 << 29))
+    b = _fitting_batch(s, pts, 1, False, seed=2) - np.array([123457, 1 << 29], np.int32)   # unshift
+    assert s.zd_insert(dev(b)) == live.insert(b)
+    assert s.zd_get_info()["fast_inserts"] == 1
+    assert_same_structure(s.zd_export(), live.tree())
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(*gpu_knn_all(s, 10), oi, od)
