@@ -626,12 +626,17 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     const void* db = nullptr;
     void* owned = nullptr;
     if ((rc = stage_in(h, batch, (size_t)m * h->dim * sizeof(int32_t), &db, &owned))) return rc;
-    // validation before any mutation.  The batch is sorted first (it only
-    // writes scratch) so that the fast-path check below shares the one sync.
+    // validation before any mutation
     rec(h, 0);
     ZD_CUDA(cudaMemsetAsync(d_invalid(h), 0, 2 * sizeof(int), h->st));   // [4] invalid, [5] fast path refused
     validate_points(h->dim, (const int32_t*)db, m, d_invalid(h), h->st);
+    ZD_CUDA(cudaMemcpyAsync(h->h_small + 4, d_invalid(h), sizeof(int), cudaMemcpyDeviceToHost, h->st));
     rec(h, 1);
+    ZD_CUDA(cudaStreamSynchronize(h->st));
+    if (h->h_small[4]) {
+        if (owned) cudaFreeAsync(owned, h->st);
+        return fail(ZD_ERANGE, "zd_insert: coordinate outside the universe box (tree unchanged)");
+    }
     const int64_t first = h->n_next;
     // sorted batch with ids first.. (K7)
     uint64_t* bk = nullptr;
@@ -641,8 +646,9 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     rec(h, 2);
     if ((rc = sort_into(h, (const int32_t*)db, m, (uint32_t)first, bk, br))) return rc;
     if (owned) cudaFreeAsync(owned, h->st);
-    // NEXT-2 fast path (incr.cu): a batch that keeps the canonical topology is applied
-    // by position shifts and a box refit instead of the full rebuild
+    // NEXT-2 fast path (incr.cu): a small batch that keeps the canonical topology is
+    // applied by position shifts and a box refit instead of the full rebuild (its
+    // check costs one more sync, so only small batches try it)
     int32_t* bleaf = nullptr;
     const bool try_fast = incr_enabled() && h->n > 1 && m <= kIncrMaxBatch;
     if (try_fast) {
@@ -651,12 +657,8 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
         t.nodes = h->tb.nodes; t.split_bit = h->tb.split_bit; t.d_meta = h->d_small; t.leaf_start = h->tb.leaf_start;
         incr_locate(h->dim, bk, m, t, h->keys, h->leaf_max, bleaf, d_invalid(h) + 1, h->st);
         ZD_CHECK_LAUNCH("incr_locate");
-    }
-    ZD_CUDA(cudaMemcpyAsync(h->h_small + 4, d_invalid(h), 2 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
-    ZD_CUDA(cudaStreamSynchronize(h->st));
-    if (h->h_small[4]) {
-        dfree(bk, h->st); dfree(br, h->st); dfree(bleaf, h->st);
-        return fail(ZD_ERANGE, "zd_insert: coordinate outside the universe box (tree unchanged)");
+        ZD_CUDA(cudaMemcpyAsync(h->h_small + 5, d_invalid(h) + 1, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+        ZD_CUDA(cudaStreamSynchronize(h->st));
     }
     const bool fast = try_fast && !h->h_small[5];
     rec(h, 3);
