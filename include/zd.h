@@ -168,6 +168,8 @@ typedef struct zd_info {
     int64_t fast_inserts; /* inserts applied without a topology rebuild (NEXT-2 fast
                              path: the batch kept the canonical topology; ZD_INCR=0
                              in the environment disables it) */
+    int64_t fast_deletes; /* deletes applied without a topology rebuild (no leaf
+                             emptied, every internal node kept > leaf_max points) */
 } zd_info;
 
 ZD_API int zd_get_info(const zd_tree *h, zd_info *out);

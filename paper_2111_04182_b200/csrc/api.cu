@@ -138,6 +138,7 @@ struct zd_tree {
     int64_t n = 0, n_next = 0, cap = 0, id_cap = 0;
     int64_t ncap = 0;   // internal-node capacity of the node-indexed tree buffers
     int64_t fast_inserts = 0;   // inserts applied by the NEXT-2 fast path (introspection/tests)
+    int64_t fast_deletes = 0;   // deletes applied by the NEXT-2 fast path
     bool shift_set = false;
     int32_t shift[3] = {0, 0, 0};   // 2D random shift, applied before encoding
     // sorted live points
@@ -725,19 +726,53 @@ int64_t zd_delete(zd_tree* h, const int32_t* ids, int64_t m) {
     compact_alive(h->alive, h->keys, h->recs, h->n, h->keys2, h->recs2, h->tb.block_cnt, h->st);
     ZD_CHECK_LAUNCH("delete");
     if (owned) cudaFreeAsync(owned, h->st);
+    // NEXT-2 delete fast path (incr.cu): checked before the count readback's sync
+    int32_t* del_before = nullptr;
+    uint32_t* dscratch = nullptr;
+    bool try_fast = incr_enabled() && m <= kIncrMaxBatch && h->n > 1;
+    if (try_fast && (rc = refresh_host_meta(h))) return rc;   // a sync only after a full rebuild
+    try_fast = try_fast && h->root >= 0;
+    if (try_fast) {
+        const int64_t nb = h->n_internal, nl = nb + 1;
+        const int64_t nblk = (nl + 255) / 256;
+        ZD_CUDA(dalloc(&del_before, nl + 1, h->st));
+        ZD_CUDA(dalloc(&dscratch, 2 * nb + nblk + 2, h->st));   // mark [nb] | arrived [nb] | bsum [nblk+1]
+        ZD_CUDA(cudaMemsetAsync(dscratch, 0, 2 * nb * sizeof(uint32_t), h->st));
+        ZD_CUDA(cudaMemsetAsync(d_invalid(h) + 1, 0, sizeof(int), h->st));
+        decr_check(nb, h->recs, h->tb.leaf_start, h->alive, h->tb.range, h->leaf_max, del_before, dscratch + 2 * nb,
+                   d_invalid(h) + 1, h->st);
+        ZD_CHECK_LAUNCH("decr_check");
+        ZD_CUDA(cudaMemcpyAsync(h->h_small + 5, d_invalid(h) + 1, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    }
     ZD_CUDA(cudaMemcpyAsync(h->h_small + 6, d_count(h), sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
     rec(h, 1);
     ZD_CUDA(cudaStreamSynchronize(h->st));
     unsigned long long cnt;
     std::memcpy(&cnt, h->h_small + 6, sizeof(cnt));
-    if (cnt == 0) return 0;
+    if (cnt == 0) {
+        dfree(del_before, h->st);
+        dfree(dscratch, h->st);
+        return 0;
+    }
+    const bool fast = try_fast && !h->h_small[5];
     std::swap(h->keys, h->keys2);
     std::swap(h->recs, h->recs2);
     h->n -= (int64_t)cnt;
     h->rows_identity = false;
     h->rows_dirty = true;
     rec(h, 2);
-    if ((rc = topology(h))) return rc;
+    if (fast) {
+        const int64_t nb = h->n_internal;
+        decr_apply(h->dim, nb, del_before, h->tb.leaf_start, h->tb.pt_leaf, h->tb.nodes, h->tb.range, h->tb.pos_range,
+                   h->tb.leaf_parent, h->recs, dscratch, dscratch + nb, h->st);
+        ZD_CHECK_LAUNCH("decr_apply");
+        h->fast_deletes += 1;
+        if (h->timing) ZD_CUDA(cudaEventRecord(h->ev[6], h->st));
+    } else if ((rc = topology(h))) {
+        return rc;
+    }
+    dfree(del_before, h->st);
+    dfree(dscratch, h->st);
     rec(h, 3);
     if (h->timing) {
         ZD_CUDA(cudaEventSynchronize(h->ev[3]));
@@ -781,6 +816,7 @@ int zd_get_info(const zd_tree* hc, zd_info* out) {
     out->node_words = h->dim == 2 ? 12 : 16;
     for (int a = 0; a < 3; ++a) out->shift[a] = h->shift[a];
     out->fast_inserts = h->fast_inserts;
+    out->fast_deletes = h->fast_deletes;
     return ZD_OK;
 }
 

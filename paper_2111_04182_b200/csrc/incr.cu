@@ -158,6 +158,132 @@ __global__ void __launch_bounds__(256) incr_refit_kernel(Node<DIM>* __restrict__
     }
 }
 
+// ---- delete fast path ------------------------------------------------------------
+// A delete batch keeps the canonical topology when no leaf is emptied and every
+// internal node keeps more than leaf_max points: then both children of every node stay
+// non-empty, so each node keeps its split bit (keys on both sides of it remain) and no
+// node collapses into a leaf.  Positions shift down; boxes shrink, so they are
+// recomputed along the paths of the leaves that lost points (a node is refit when its
+// last dirty child arrives).
+
+// per leaf: dead records (old positions, alive bitset by id), emptied-leaf check,
+// block-exclusive scan into del_before, block totals into bsum
+__global__ void __launch_bounds__(256) decr_count_kernel(const int4* __restrict__ recs,
+                                                         const int32_t* __restrict__ leaf_start, int32_t nleaves,
+                                                         const uint32_t* __restrict__ alive, int32_t* __restrict__ del_before,
+                                                         uint32_t* __restrict__ bsum, int* __restrict__ bad) {
+    __shared__ uint32_t s_warp[32];
+    const int32_t l = blockIdx.x * 256 + threadIdx.x;
+    uint32_t c = 0;
+    if (l < nleaves) {
+        const int32_t s = __ldg(leaf_start + l), e = __ldg(leaf_start + l + 1);
+        for (int32_t p = s; p < e; ++p) {
+            const int32_t id = __ldg(recs + p).w;
+            c += ((__ldg(alive + (id >> 5)) >> (id & 31)) & 1u) ? 0u : 1u;
+        }
+        if ((int32_t)c == e - s) atomicOr(bad, 1);   // leaf emptied
+    }
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan<256>(c, s_warp, &total);
+    if (l < nleaves) del_before[l] = (int32_t)ex;
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+// del_before[l] += block offset; del_before[nleaves] = total
+__global__ void __launch_bounds__(256) decr_fix_kernel(int32_t* __restrict__ del_before, int32_t nleaves,
+                                                       const uint32_t* __restrict__ bsum, uint32_t nblocks) {
+    const int32_t l = blockIdx.x * 256 + threadIdx.x;
+    if (l < nleaves) del_before[l] += (int32_t)__ldg(bsum + (l >> 8));
+    else if (l == nleaves) del_before[l] = (int32_t)__ldg(bsum + nblocks);
+}
+
+// every internal node keeps > leaf_max points
+__global__ void __launch_bounds__(256) decr_check_kernel(int32_t nb, const int32_t* __restrict__ range,
+                                                         const int32_t* __restrict__ leaf_start,
+                                                         const int32_t* __restrict__ del_before, int leaf_max,
+                                                         int* __restrict__ bad) {
+    const int32_t i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= nb) return;
+    const int32_t L = __ldg(range + 2 * i), R = __ldg(range + 2 * i + 1);
+    const int32_t size = __ldg(leaf_start + R + 1) - __ldg(leaf_start + L);
+    const int32_t del = __ldg(del_before + R + 1) - __ldg(del_before + L);
+    if (size - del <= leaf_max) atomicOr(bad, 1);
+}
+
+__global__ void __launch_bounds__(256) decr_leaf_start_kernel(int32_t* __restrict__ leaf_start, int32_t nleaves,
+                                                              const int32_t* __restrict__ del_before) {
+    const int32_t l = blockIdx.x * 256 + threadIdx.x;
+    if (l <= nleaves) leaf_start[l] -= __ldg(del_before + l);
+}
+
+// mark, for each node, which children lie on a dirty leaf's path (bit 0 left, 1 right)
+template <int DIM>
+__global__ void __launch_bounds__(256) decr_mark_kernel(const Node<DIM>* __restrict__ nodes,
+                                                        const int32_t* __restrict__ leaf_parent,
+                                                        const int32_t* __restrict__ del_before, int32_t nleaves,
+                                                        uint32_t* __restrict__ mark) {
+    const int32_t l = blockIdx.x * 256 + threadIdx.x;
+    if (l >= nleaves || __ldg(del_before + l + 1) == __ldg(del_before + l)) return;
+    int32_t P = __ldg(leaf_parent + l), C = -1;
+    uint32_t side = P == l ? 1u : 2u;   // leaf l is the left child of node l
+    while (P >= 0) {
+        if (atomicOr(mark + P, side) != 0u) break;   // the path above is marked already
+        C = P;
+        P = __ldg(&nodes[C].parent);
+        if (P >= 0) side = __ldg(&nodes[P].left) == C ? 1u : 2u;
+    }
+}
+
+template <int DIM>
+__device__ __forceinline__ void put_box(typename BoxT<DIM>::T* dst, const typename BoxT<DIM>::T (&b)[2 * DIM]) {
+#pragma unroll
+    for (int a = 0; a < 2 * DIM; ++a) dst[a] = b[a];
+}
+
+// recompute dirty leaf boxes from the compacted records and refit up the marked paths
+template <int DIM>
+__global__ void __launch_bounds__(256) decr_refit_kernel(Node<DIM>* nodes, const int32_t* __restrict__ leaf_parent,
+                                                         const int32_t* __restrict__ leaf_start_new,
+                                                         const int32_t* __restrict__ del_before, int32_t nleaves,
+                                                         const int4* __restrict__ recs, const uint32_t* __restrict__ mark,
+                                                         uint32_t* arrived) {
+    using T = typename BoxT<DIM>::T;
+    const int32_t l = blockIdx.x * 256 + threadIdx.x;
+    if (l >= nleaves || __ldg(del_before + l + 1) == __ldg(del_before + l)) return;
+    int32_t lo[DIM], hi[DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) { lo[a] = INT32_MAX; hi[a] = INT32_MIN; }
+    const int32_t e = __ldg(leaf_start_new + l + 1);
+    for (int32_t p = __ldg(leaf_start_new + l); p < e; ++p) {
+        const int4 r = __ldg(recs + p);
+        const int c[3] = {r.x, r.y, r.z};
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) { lo[a] = min(lo[a], c[a]); hi[a] = max(hi[a], c[a]); }
+    }
+    T b[2 * DIM];
+#pragma unroll
+    for (int a = 0; a < DIM; ++a) { b[a] = (T)lo[a]; b[DIM + a] = (T)hi[a]; }
+    int32_t P = __ldg(leaf_parent + l), C = -1;
+    bool left = P == l;
+    while (P >= 0) {
+        put_box<DIM>(left ? nodes[P].lbox : nodes[P].rbox, b);
+        __threadfence();   // release: the box before the arrival
+        const uint32_t need = __popc(__ldcg(mark + P));
+        if (atomicAdd(arrived + P, 1u) + 1u < need) return;   // the other dirty child finishes P
+        __threadfence();   // acquire: the sibling's box
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            const T l0 = __ldcg(nodes[P].lbox + a), r0 = __ldcg(nodes[P].rbox + a);
+            const T l1 = __ldcg(nodes[P].lbox + DIM + a), r1 = __ldcg(nodes[P].rbox + DIM + a);
+            b[a] = l0 < r0 ? l0 : r0;
+            b[DIM + a] = l1 > r1 ? l1 : r1;
+        }
+        C = P;
+        P = __ldcg(&nodes[C].parent);
+        if (P >= 0) left = __ldcg(&nodes[P].left) == C;
+    }
+}
+
 }  // namespace
 
 void incr_locate(int dim, const uint64_t* bkeys, int64_t m, const KnnArgs& t, const uint64_t* keys, int leaf_max,
@@ -189,6 +315,43 @@ void incr_apply(int dim, int64_t nb, const int32_t* bleaf, const int4* brecs, in
     } else {
         incr_nodes_kernel<3><<<gn, 256, 0, st>>>((Node<3>*)nodes, (int32_t)nb, leaf_start, range, pos_range);
         incr_refit_kernel<3><<<gm, 256, 0, st>>>((Node<3>*)nodes, leaf_parent, bleaf, brecs, (int32_t)m);
+    }
+}
+
+}  // namespace zd
+
+namespace zd {
+
+int decr_check(int64_t nb, const int4* recs_old, const int32_t* leaf_start, const uint32_t* alive,
+               const int32_t* range, int leaf_max, int32_t* del_before, uint32_t* bsum, int* bad, cudaStream_t st) {
+    const int32_t nleaves = (int32_t)nb + 1;
+    const uint32_t nblk = (uint32_t)((nleaves + 255) / 256);
+    count_launch(4);
+    decr_count_kernel<<<nblk, 256, 0, st>>>(recs_old, leaf_start, nleaves, alive, del_before, bsum, bad);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>(bsum, nblk);
+    decr_fix_kernel<<<(nleaves + 1 + 255) / 256, 256, 0, st>>>(del_before, nleaves, bsum, nblk);
+    if (nb > 0) decr_check_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>((int32_t)nb, range, leaf_start, del_before, leaf_max, bad);
+    return 0;
+}
+
+void decr_apply(int dim, int64_t nb, const int32_t* del_before, int32_t* leaf_start, int32_t* pt_leaf, void* nodes,
+                const int32_t* range, int2* pos_range, const int32_t* leaf_parent, const int4* recs_new, uint32_t* mark,
+                uint32_t* arrived, cudaStream_t st) {
+    const int32_t nleaves = (int32_t)nb + 1;
+    const unsigned gl = (unsigned)((nleaves + 255) / 256), gn = (unsigned)std::max<int64_t>(1, (nb + 255) / 256);
+    count_launch(5);
+    decr_leaf_start_kernel<<<(nleaves + 1 + 255) / 256, 256, 0, st>>>(leaf_start, nleaves, del_before);
+    incr_pt_leaf_kernel<<<gl, 256, 0, st>>>(leaf_start, nleaves, pt_leaf);
+    if (dim == 2) {
+        incr_nodes_kernel<2><<<gn, 256, 0, st>>>((Node<2>*)nodes, (int32_t)nb, leaf_start, range, pos_range);
+        decr_mark_kernel<2><<<gl, 256, 0, st>>>((const Node<2>*)nodes, leaf_parent, del_before, nleaves, mark);
+        decr_refit_kernel<2><<<gl, 256, 0, st>>>((Node<2>*)nodes, leaf_parent, leaf_start, del_before, nleaves, recs_new,
+                                                 mark, arrived);
+    } else {
+        incr_nodes_kernel<3><<<gn, 256, 0, st>>>((Node<3>*)nodes, (int32_t)nb, leaf_start, range, pos_range);
+        decr_mark_kernel<3><<<gl, 256, 0, st>>>((const Node<3>*)nodes, leaf_parent, del_before, nleaves, mark);
+        decr_refit_kernel<3><<<gl, 256, 0, st>>>((Node<3>*)nodes, leaf_parent, leaf_start, del_before, nleaves, recs_new,
+                                                 mark, arrived);
     }
 }
 

@@ -91,6 +91,15 @@ void incr_locate(int dim, const uint64_t* bkeys, int64_t m, const KnnArgs& t, co
 void incr_apply(int dim, int64_t nb, const int32_t* bleaf, const int4* brecs, int64_t m, int32_t* leaf_start,
                 int32_t* pt_leaf, void* nodes, const int32_t* range, int2* pos_range, const int32_t* leaf_parent,
                 cudaStream_t st);
+// Delete fast path: dead records per leaf (old arrays + alive bitset) scanned into
+// del_before [nleaves+1] (bsum: block scratch), *bad if a leaf empties or an internal
+// node drops to <= leaf_max points; then the position shifts and dirty-path box refit
+// (mark, arrived: zeroed node-sized scratch).
+int decr_check(int64_t nb, const int4* recs_old, const int32_t* leaf_start, const uint32_t* alive,
+               const int32_t* range, int leaf_max, int32_t* del_before, uint32_t* bsum, int* bad, cudaStream_t st);
+void decr_apply(int dim, int64_t nb, const int32_t* del_before, int32_t* leaf_start, int32_t* pt_leaf, void* nodes,
+                const int32_t* range, int2* pos_range, const int32_t* leaf_parent, const int4* recs_new, uint32_t* mark,
+                uint32_t* arrived, cudaStream_t st);
 // Work counters of the packet k-NN kernel (only in a -DZD_KNN_STATS build).
 enum { ZS_PACKETS = 0, ZS_QUERIES, ZS_NODES, ZS_POPS, ZS_ASCENTS, ZS_SPANS, ZS_PASSES, ZS_CAND, ZS_HITS,
        ZS_ROUNDS, ZS_COMPACT, ZS_SURV, ZS_SURV_MAX, ZS_CYCLES, ZS_MAXPKT, ZS_DEFERRED, ZS_HIST0, ZD_NSTATS = ZS_HIST0 + 32 };

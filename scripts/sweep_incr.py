@@ -2,8 +2,9 @@
 
 For batches that keep the canonical topology (points placed in leaves with room:
 copies of a leaf's point with the lowest bit of one coordinate flipped), time the
-insert with the fast path and with ZD_INCR=0 (full rebuild), m = 100 .. 64K; and the
-fraction of random uniform single-point inserts that keep the topology.  One JSON line
+insert with the fast path and with ZD_INCR=0 (full rebuild), m = 100 .. 64K, and the
+delete of those points again; and the fraction of random single-point inserts and
+deletes that keep the topology.  One JSON line
 per measurement."""
 import json
 import os
@@ -60,6 +61,30 @@ for name in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["C3", "C2"]):
         print(json.dumps({"config": name, "batch": m, "fast_ms": round(ms_f, 4), "rebuild_ms": round(ms_r, 4),
                           "fast_path_taken": bool(nf), "fast_ns_per_point": round(ms_f * 1e6 / m, 1),
                           "rebuild_ns_per_point": round(ms_r * 1e6 / m, 1)}), flush=True)
+    # deletes that undo a fitting insert (keep the topology) vs the rebuild
+    for m in (100, 1000, 10000):
+        b = torch.from_numpy(fitting(ex, dim, m, rng)).cuda()
+        res = {}
+        for incr in (True, False):
+            os.environ["ZD_INCR"] = "1" if incr else "0"
+            best, fd = 1e9, 0
+            for _ in range(3):
+                t3 = zd.zd_build(pts)
+                first = t3.zd_insert(b)
+                ids = torch.arange(first, first + m, dtype=torch.int32, device="cuda")
+                d0 = t3.zd_get_info()["fast_deletes"]
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                e0.record()
+                t3.zd_delete(ids)
+                e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+                fd = t3.zd_get_info()["fast_deletes"] - d0
+                t3.zd_free()
+            res[incr] = (best, fd)
+        print(json.dumps({"config": name, "delete_batch": m, "fast_ms": round(res[True][0], 4),
+                          "rebuild_ms": round(res[False][0], 4), "fast_path_taken": bool(res[True][1])}), flush=True)
     # how often does a random single point keep the topology?
     os.environ["ZD_INCR"] = "1"
     t2 = zd.zd_build(pts)
@@ -69,3 +94,9 @@ for name in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["C3", "C2"]):
         t2.zd_insert(torch.from_numpy(q[i:i + 1]).cuda())
     frac = (t2.zd_get_info()["fast_inserts"] - f0) / len(q)
     print(json.dumps({"config": name, "random_single_point_inserts": len(q), "fraction_fast": round(frac, 3)}), flush=True)
+    d0 = t2.zd_get_info()["fast_deletes"]
+    kill = np.random.default_rng(9).choice(pts_np.shape[0], size=300, replace=False).astype(np.int32)
+    for i in range(len(kill)):
+        t2.zd_delete(torch.from_numpy(kill[i:i + 1]).cuda())
+    frac = (t2.zd_get_info()["fast_deletes"] - d0) / len(kill)
+    print(json.dumps({"config": name, "random_single_point_deletes": len(kill), "fraction_fast": round(frac, 3)}), flush=True)

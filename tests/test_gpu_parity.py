@@ -626,3 +626,44 @@ def test_insert_fast_path_disabled_and_shifted(zd, oracle_mod, monkeypatch):
     assert_same_structure(s.zd_export(), live.tree())
     oi, od, _ = live.tree().knn_all(10)
     check_rows(*gpu_knn_all(s, 10), oi, od)
+
+
+@pytest.mark.parametrize("dist,dim", [("uniform", 3), ("plummer", 3), ("uniform", 2), ("kuzmin", 2)])
+def test_delete_fast_path(zd, oracle_mod, monkeypatch, dist, dim):
+    """Deletes that keep the topology (no leaf emptied, every internal node keeps more
+    than leaf_max points) shift positions and refit the dirty paths' boxes instead of
+    rebuilding: removing points added by a fitting insert restores the original tree."""
+    monkeypatch.delenv("ZD_INCR", raising=False)
+    pts = zdgen.points(dist, 40000, dim, seed=93)
+    t = zd.zd_build(dev(pts))
+    live = oracle_mod.LiveSet(pts)
+    before = t.zd_export()
+    b = _fitting_batch(t, pts, 1, True, seed=11)
+    first = t.zd_insert(dev(b))
+    assert first == live.insert(b)
+    new_ids = np.arange(first, first + len(b), dtype=np.int32)
+    d0 = t.zd_get_info()["fast_deletes"]
+    for part in np.array_split(new_ids, 3):
+        assert t.zd_delete(dev(part)) == live.delete(part) == len(part)
+        assert_same_structure(t.zd_export(), live.tree())
+    assert t.zd_get_info()["fast_deletes"] - d0 == 3
+    after = t.zd_export()
+    assert np.array_equal(after["nodes"], before["nodes"]) and np.array_equal(after["leaf_start"], before["leaf_start"])
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(gi, gd, oi, od)
+    # single random deletes: fast or rebuilt, always canonical
+    rng = np.random.default_rng(3)
+    for r in range(6):
+        kill = rng.choice(live.live_ids(), size=1 + r % 3, replace=False).astype(np.int32)
+        assert t.zd_delete(dev(kill)) == live.delete(kill)
+        assert_same_structure(t.zd_export(), live.tree())
+    # a batch that empties nodes falls back to the rebuild
+    kill = live.live_ids()[:3000].astype(np.int32)
+    f = t.zd_get_info()["fast_deletes"]
+    assert t.zd_delete(dev(kill)) == live.delete(kill)
+    assert t.zd_get_info()["fast_deletes"] == f
+    assert_same_structure(t.zd_export(), live.tree())
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(gi, gd, oi, od)
