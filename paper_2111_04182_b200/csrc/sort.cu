@@ -22,7 +22,7 @@ namespace {
 
 constexpr int ST = 256;              // threads per tile
 #ifndef ZD_SORT_SI
-#define ZD_SORT_SI 11
+#define ZD_SORT_SI 13
 #endif
 #ifndef ZD_SORT_MINB
 #define ZD_SORT_MINB 4

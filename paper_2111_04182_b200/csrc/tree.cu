@@ -34,7 +34,10 @@ namespace zd {
 namespace {
 
 constexpr int TT = 256;
-constexpr int TPI = 4;
+#ifndef ZD_TPI
+#define ZD_TPI 4
+#endif
+constexpr int TPI = ZD_TPI;   // pairs per thread in the flags / compact kernels
 constexpr int TTILE = TT * TPI;   // pairs per block
 constexpr int HALO = kMaxLeaf;
 
