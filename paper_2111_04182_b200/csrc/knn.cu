@@ -195,7 +195,7 @@ struct Cap {   // buffered candidates per lane (overflow compacts per lane: any 
 #define ZD_COARSE 32    // 2D
 #endif
 #ifndef ZD_COARSE3
-#define ZD_COARSE3 64   // 3D (with the fp32 prefilter wide spans are cheap)
+#define ZD_COARSE3 96   // 3D (with the fp32 prefilter wide spans are cheap)
 #endif
 struct Ref {
     int32_t ref, s, e;
@@ -386,7 +386,7 @@ __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Qu
 #define ZD_TRANSPOSE_MAX 6   // 2D: at most this many needing lanes: lanes = candidates
 #endif
 #ifndef ZD_TRANSPOSE_MAX3
-#define ZD_TRANSPOSE_MAX3 2  // 3D
+#define ZD_TRANSPOSE_MAX3 3  // 3D
 #endif
 template <int DIM>
 struct TMax {
