@@ -166,7 +166,10 @@ __device__ __forceinline__ void store_box(typename BoxT<DIM>::T* dst, const int3
 // protocol.  A node's range is bounded by the nearest larger split bit on each side
 // (the canonical tree is the Cartesian tree of the split bits), found by scanning the
 // window's split bits in shared memory.
-constexpr int BW = 128;
+#ifndef ZD_BU_WINDOW
+#define ZD_BU_WINDOW 128
+#endif
+constexpr int BW = ZD_BU_WINDOW;   // leaves per bottom-up block (window)
 #ifndef ZD_LEAF_UNROLL
 #define ZD_LEAF_UNROLL 4
 #endif
