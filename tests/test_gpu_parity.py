@@ -29,7 +29,8 @@ def check_rows(gi, gd, oi, od):
     assert bad.size == 0, f"{bad.size} rows differ, first row {bad[0]}: gpu {gi[bad[0]]} {gd[bad[0]]} oracle {oi[bad[0]]} {od[bad[0]]}"
 
 
-SIZES = [0, 1, 2, 3, 16, 17, 33, 1000, 2815, 2816, 2817, 3327, 3328, 3329, 6657, 20011]   # sort tile: 13 x 256 keys
+# one-sweep tiles of 13 x 256 = 3328 keys
+SIZES = [0, 1, 2, 3, 16, 17, 33, 1000, 2047, 2048, 2049, 2815, 2816, 2817, 3327, 3328, 3329, 6657, 20011]
 
 
 @pytest.mark.parametrize("n", SIZES)
