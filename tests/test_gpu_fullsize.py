@@ -82,3 +82,34 @@ def test_config_full_external(zd, oracle_mod, name):
     rows = np.sort(np.random.default_rng(7).choice(len(q), size=500, replace=False))
     bi, bd = oracle_mod.brute_knn(pts, None, q[rows], None, K)
     assert np.array_equal(gi.cpu().numpy()[rows], bi) and np.array_equal(gd.cpu().numpy()[rows], bd)
+
+
+def test_config_full_fast_updates(zd, oracle_mod, monkeypatch):
+    """NEXT-2 fast paths at full size (C3, 10M): 1,000 points placed in leaves with room
+    take the insert fast path; 300 sampled rows vs brute force; deleting them again
+    takes the delete fast path and restores the original tree exactly."""
+    monkeypatch.delenv("ZD_INCR", raising=False)
+    pts = zdgen.config_points("C3")
+    t = zd.zd_build(torch.from_numpy(pts).cuda())
+    ex = t.zd_export()
+    ls = ex["leaf_start"]
+    rng = np.random.default_rng(12)
+    leaves = rng.choice(np.nonzero(np.diff(ls) <= 15)[0], size=1000, replace=False)
+    b = ex["recs"][ls[leaves], :3].astype(np.int64)
+    b[np.arange(1000), rng.integers(0, 3, size=1000)] ^= 1
+    b = np.ascontiguousarray(b.astype(np.int32))
+    first = t.zd_insert(torch.from_numpy(b).cuda())
+    assert first == len(pts) and t.zd_get_info()["fast_inserts"] == 1
+    allp = np.concatenate([pts, b])
+    gi, gd = t.zd_knn(K)
+    torch.cuda.synchronize()
+    rows = np.sort(np.concatenate([rng.choice(len(pts), size=200, replace=False),
+                                   len(pts) + rng.choice(1000, size=100, replace=False)])).astype(np.int32)
+    bi, bd = oracle_mod.brute_knn(allp, None, allp[rows], rows, K)
+    sel = torch.from_numpy(rows).long().cuda()
+    assert np.array_equal(gi[sel].cpu().numpy(), bi) and np.array_equal(gd[sel].cpu().numpy(), bd)
+    ids = torch.arange(first, first + 1000, dtype=torch.int32, device="cuda")
+    assert t.zd_delete(ids) == 1000 and t.zd_get_info()["fast_deletes"] == 1
+    ex2 = t.zd_export()
+    for key in ("keys", "recs", "leaf_start", "leaf_parent", "nodes"):
+        assert np.array_equal(ex2[key], ex[key]), key
