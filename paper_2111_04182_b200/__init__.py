@@ -245,7 +245,8 @@ class ZdTree:
 
 
 KNN_STATS = ("packets", "queries", "nodes", "pops", "ascents", "spans", "passes", "candidates", "hits",
-             "rounds", "compactions", "survivors", "survivors_max", "cycles", "max_packet", "deferred") + tuple(f"hist{i}" for i in range(32))
+             "rounds", "compactions", "survivors", "survivors_max", "cycles", "max_packet", "deferred") + tuple(f"hist{i}" for i in range(32)) + (
+    "insertions", "seed_hits", "seed_insertions", "seed_rounds", "lane_compactions")
 
 
 def zd_knn_stats(reset: bool = True) -> dict:

@@ -3,7 +3,9 @@ with the repo snapshot to the GPU box)."""
 from __future__ import annotations
 
 import os
+import shutil
 import subprocess
+import tempfile
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -38,15 +40,30 @@ def stale(path: Path = LIB_PATH) -> bool:
 
 
 def build_lib(force: bool = False, verbose: bool = False, stats: bool = False, defines=(), out=None) -> Path:
-    """Build libzd.so (or, for experiments, a variant with extra -D defines at `out`)."""
+    """Build libzd.so (or, for experiments, a variant with extra -D defines at `out`).
+    Each translation unit is compiled in parallel (nvcc -c), then linked with nvcc."""
     path = Path(out).resolve() if out else (STATS_LIB_PATH if stats else LIB_PATH)
     if not force and not stale(path):
         return path
+    tag = f"{path.stem}.{os.getpid()}"
+    objdir = Path(tempfile.mkdtemp(prefix=f"zdobj_{tag}_"))
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    extra = [*(["-DZD_KNN_STATS"] if stats else []), *[f"-D{d}" for d in defines]]
+    procs = []
+    for s in SOURCES:
+        cmd = [_nvcc(), *flags, *extra, "-c", str(CSRC / s), "-o", str(objdir / (s + ".o"))]
+        if verbose:
+            print(" ".join(cmd))
+        procs.append((cmd, subprocess.Popen(cmd, cwd=str(CSRC))))
+    for cmd, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, cmd)
     tmp = path.with_name(f"{path.name}.tmp{os.getpid()}")
-    cmd = [_nvcc(), *NVCC_FLAGS, *(["-DZD_KNN_STATS"] if stats else []), *[f"-D{d}" for d in defines],
-           *[str(CSRC / s) for s in SOURCES], "-o", str(tmp)]
+    link = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+            *[str(objdir / (s + ".o")) for s in SOURCES], "-o", str(tmp)]
     if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd, cwd=str(CSRC))
+        print(" ".join(link))
+    subprocess.check_call(link, cwd=str(CSRC))
     os.replace(tmp, path)
+    shutil.rmtree(objdir, ignore_errors=True)
     return path

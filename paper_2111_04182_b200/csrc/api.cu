@@ -321,6 +321,10 @@ void elapsed(zd_tree* h, int phase, int a, int b) {
     if (h->timing && cudaEventElapsedTime(&t, h->ev[a], h->ev[b]) == cudaSuccess) h->ms[phase] = t;
 }
 
+// Largest key count of one radix sort (sort.cu: 30-bit digit counts in the look-back
+// status words).  Builds, insert batches and external query sets stay below it.
+constexpr int64_t kMaxSortKeys = (int64_t)1 << 30;
+
 // NEXT-2 insert fast path: batches up to this size are checked; ZD_INCR=0 disables it.
 constexpr int64_t kIncrMaxBatch = (int64_t)1 << 16;
 bool incr_enabled() {
@@ -440,7 +444,8 @@ int zd_last_error_code(void) { return g_err_code; }
 zd_tree* zd_build_ex(const int32_t* points, int64_t n, int dim, const zd_opts* opts) {
     clear_err();
     if (dim != 2 && dim != 3) { fail(ZD_EINVAL, "zd_build: dim must be 2 or 3"); return nullptr; }
-    if (n < 0 || n >= ((int64_t)1 << 31) - 1) { fail(ZD_EINVAL, "zd_build: need 0 <= n < 2^31-1"); return nullptr; }
+    // the radix sort's look-back words carry 30-bit digit counts: one sort holds < 2^30 keys
+    if (n < 0 || n >= kMaxSortKeys) { fail(ZD_EINVAL, "zd_build: need 0 <= n < 2^30"); return nullptr; }
     if (n > 0 && !points) { fail(ZD_EINVAL, "zd_build: points is NULL"); return nullptr; }
     int leaf_max = 16;
     cudaStream_t st = nullptr;
@@ -523,7 +528,8 @@ int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out
     if (flags & ~(ZD_KNN_ROOT_BASED | ZD_KNN_WARP)) return fail(ZD_EINVAL, "zd_knn_ex: unknown flags");
     if (!h) return fail(ZD_EINVAL, "NULL handle");
     if (k < 1 || k > ZD_K_MAX) return fail(ZD_EINVAL, "zd_knn: k must be in [1, ZD_K_MAX]");
-    if (m < 0 || m >= ((int64_t)1 << 31) - 1) return fail(ZD_EINVAL, "zd_knn: bad m");
+    if (m < 0 || (queries ? m >= kMaxSortKeys : m >= ((int64_t)1 << 31) - 1))
+        return fail(ZD_EINVAL, "zd_knn: bad m (external queries: m < 2^30)");
     if (!queries && m != h->n) return fail(ZD_EINVAL, "zd_knn: all-points query needs m == zd_size(h)");
     if (m > 0 && (!out_idx || !out_dist2)) return fail(ZD_EINVAL, "zd_knn: NULL output");
     if (m == 0) return ZD_OK;
@@ -619,7 +625,7 @@ int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out
 int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     clear_err();
     if (!h) return fail(ZD_EINVAL, "NULL handle");
-    if (m < 0) return fail(ZD_EINVAL, "zd_insert: m < 0");
+    if (m < 0 || m >= kMaxSortKeys) return fail(ZD_EINVAL, "zd_insert: need 0 <= m < 2^30");
     if (m == 0) return h->n_next;
     if (!batch) return fail(ZD_EINVAL, "zd_insert: batch is NULL");
     if (h->n_next + m >= ((int64_t)1 << 31) - 1) return fail(ZD_EINVAL, "zd_insert: id space exhausted (2^31)");
@@ -651,7 +657,9 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     // applied by position shifts and a box refit instead of the full rebuild (its
     // check costs one more sync, so only small batches try it)
     int32_t* bleaf = nullptr;
-    const bool try_fast = incr_enabled() && h->n > 1 && m <= kIncrMaxBatch;
+    bool try_fast = incr_enabled() && h->n > 1 && m <= kIncrMaxBatch;
+    if (try_fast && (rc = refresh_host_meta(h))) return rc;   // valid after a build: no sync
+    try_fast = try_fast && h->root >= 0;                     // a single-leaf tree rebuilds
     if (try_fast) {
         ZD_CUDA(dalloc(&bleaf, m, h->st));
         KnnArgs t{};

@@ -37,7 +37,11 @@ __global__ void __launch_bounds__(256) incr_locate_kernel(const uint64_t* __rest
     if (i >= m) return;
     const uint64_t key = __ldg(bkeys + i);
     int32_t cur = __ldg(meta + 1);
-    if (cur < 0) { atomicOr(bad, 1); return; }   // single-leaf tree: full rebuild
+    if (cur < 0) {   // single-leaf tree: full rebuild (bleaf stays a valid leaf index)
+        bleaf[i] = 0;
+        atomicOr(bad, 1);
+        return;
+    }
     int32_t leaf = 0, pb = 0;
     while (true) {
         pb = __ldg(split_bit + cur);
@@ -66,7 +70,7 @@ __global__ void __launch_bounds__(256) incr_check_kernel(const int32_t* __restri
                                                          const int32_t* __restrict__ leaf_start, int leaf_max,
                                                          int* __restrict__ bad) {
     const int32_t i = blockIdx.x * 256 + threadIdx.x;
-    if (i >= m) return;
+    if (i >= m || *(volatile int*)bad) return;   // refused already: leaf indices need not be valid
     const int32_t l = __ldg(bleaf + i);
     if (i > 0 && __ldg(bleaf + i - 1) > l) { atomicOr(bad, 1); return; }
     if (i == 0 || __ldg(bleaf + i - 1) != l) {   // first batch key of leaf l counts the leaf

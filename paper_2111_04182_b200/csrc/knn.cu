@@ -257,6 +257,11 @@ struct WarpSh {
 #endif
 };
 
+#ifndef ZD_SEEDW
+#define ZD_SEEDW 12      // window seed half-width (all-points queries)
+#endif
+constexpr int kSeedW = ZD_SEEDW;
+
 template <int DIM, int K>
 struct Lane {
     Query<DIM> q;
@@ -265,6 +270,10 @@ struct Lane {
     float qf[3];        // 3D fp32 filter: the query in fp32 (exact)
     float wb;           //   and a bound with d2 <= U  =>  fp32 d2 <= wb
     int cnt;
+    int32_t wlo;        // window seed: positions [wlo, wlo + 2 * SeedW] were scanned already
+#ifdef ZD_KNN_STATS
+    bool seed;          // profiling: inside the seed scan
+#endif
 };
 
 template <int DIM, int K>
@@ -354,6 +363,16 @@ __device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<DIM, K>& S, int 
         w += (f <= F) ? 1 : 0;
     }
     L.cnt = w;
+}
+
+// Insert xf into the sorted list fa, dropping the largest: every new slot is the
+// median of (fa[t-1], xf, fa[t]) — all slots independent (depth 2) instead of a
+// K-long compare-exchange chain.  xf >= fa[K-1] leaves fa unchanged.
+template <int K>
+__device__ __forceinline__ void fa_insert(float (&fa)[K], float xf) {
+#pragma unroll
+    for (int t = K - 1; t > 0; --t) fa[t] = fmaxf(fa[t - 1], fminf(fa[t], xf));
+    fa[0] = fminf(fa[0], xf);
 }
 
 // Rare path (massive distance ties survive compaction): keep only the exact K best
@@ -584,6 +603,19 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                     }
                 }
             }
+            {
+                // drop the staged slots of the lane's window seed (scanned already): the
+                // window is a contiguous range of raw offsets of this chunk, so its staged
+                // slots (compacted in order by km) are contiguous too
+                const int32_t lo_r = L.wlo - b, hi_r = L.wlo + 2 * kSeedW + 1 - b;   // raw [lo_r, hi_r)
+                const bool inw = lo_r < 32 && hi_r > 0;
+                if (__any_sync(0xffffffffu, inw) && inw) {
+                    const int a = max(lo_r, 0), z = min(hi_r, 32);
+                    const int sa = __popc(km & ((1u << a) - 1u));
+                    const int sz = __popc(z >= 32 ? km : (km & ((1u << z) - 1u)));
+                    hit &= ~((sz >= 32 ? 0xffffffffu : ((1u << sz) - 1u)) & ~((1u << sa) - 1u));
+                }
+            }
 #ifdef ZD_KNN_STATS
             {
                 ZD_STAT(ZS_CAND, cnt);
@@ -592,31 +624,35 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 for (int o = 16; o > 0; o >>= 1) { hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o)); hc += __shfl_xor_sync(0xffffffffu, hc, o); }
                 ZD_STAT(ZS_HITS, hc);
                 ZD_STAT(ZS_ROUNDS, hm);
+                if (L.seed) { ZD_STAT(ZS_SEED_HITS, hc); ZD_STAT(ZS_SEED_ROUNDS, hm); }
             }
 #endif
             while (hit) {
                 const int j = h0 + __ffs(hit) - 1;
                 hit &= hit - 1;
                 float xf;
+                bool stale;   // outside the lane's current bound (it shrank since the test)
                 if constexpr (DIM == 3) {
                     const float4 c = S.f[j];
                     const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
                     const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                    // the bound shrank since the test, or self (excluded by id, reading 13)
-                    if (df > L.wb || __float_as_int(c.w) == L.q.id) continue;
+                    if (__float_as_int(c.w) == L.q.id) continue;   // self (excluded by id, reading 13)
+                    stale = df > L.wb;
                     xf = __fmul_ru(df, 1.0f + 0x1p-21f);   // >= the exact d2
                 } else {
                     const int4 c = S.c[j];
+                    if (c.w == L.q.id) continue;   // self
                     const int64_t d = dist2<DIM>(L.q, c);
-                    if (d > L.U || c.w == L.q.id) continue;   // bound shrank since the test, or self
+                    stale = d > L.U;
                     xf = __ll2float_ru(d);
                 }
-                // sorted insertion of xf, dropping the largest: every new slot is the
-                // median of (fa[t-1], xf, fa[t]) — all slots independent (depth 2)
-                // instead of a K-long compare-exchange chain
-#pragma unroll
-                for (int t = K - 1; t > 0; --t) L.fa[t] = fmaxf(L.fa[t - 1], fminf(L.fa[t], xf));
-                L.fa[0] = fminf(L.fa[0], xf);
+                if (stale) continue;
+#ifdef ZD_KNN_STATS
+                atomicAdd(&g_knn_stats[ZS_INS], 1ull);
+                if (L.seed) atomicAdd(&g_knn_stats[ZS_SEED_INS], 1ull);
+                if (L.cnt == Cap<DIM, K>::v) atomicAdd(&g_knn_stats[ZS_LANE_COMPACT], 1ull);
+#endif
+                fa_insert<K>(L.fa, xf);
                 set_bound<DIM, K>(L);
                 if (L.cnt == Cap<DIM, K>::v) {   // rare: per-lane compaction
                     compact<DIM, K>(L, S, lane);
@@ -631,6 +667,162 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
             }
         }
     }
+}
+
+// Seed (Alg. 3's leaf scan, for the whole packet): every lane tests every
+// record of [s, e) (the packet's leaves and their neighbours).  Early in a search
+// almost every candidate improves the k-best list, so instead of per-hit divergent
+// insertions the seed runs two warp-uniform passes:
+//   1. fold every candidate's ru(d2) into fa (the branch-free median insertion is a
+//      no-op for a value >= fa[K-1]; skipped when no lane would change);
+//   2. with the bound of step 1, buffer every candidate within it (the same test as
+//      the hit path), so the buffer receives ~k entries and never the whole seed.
+// Self (by id, reading 13) and idle lanes take +inf in step 1 and are never buffered.
+template <int DIM, int K>
+__device__ __forceinline__ void seed_scan(const int4* __restrict__ recs, int32_t s, int32_t e, bool active,
+                                          Lane<DIM, K>& L, WarpSh<DIM, K>& S, int lane) {
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll 1
+        for (int32_t b = s; b < e; b += 32) {
+            const int n32 = min(32, e - b);
+            __syncwarp();
+            if (lane < n32) {
+                const int4 r = __ldg(recs + b + lane);
+                if constexpr (DIM == 3)
+                    S.f[lane] = make_float4(__int2float_rn(r.x), __int2float_rn(r.y), __int2float_rn(r.z), __int_as_float(r.w));
+                else
+                    S.c[lane] = r;
+            }
+            __syncwarp();
+            if (pass == 0) {
+#pragma unroll 1
+                for (int j = 0; j < n32; ++j) {
+                    float xf;
+                    int32_t cid;
+                    if constexpr (DIM == 3) {
+                        const float4 c = S.f[j];
+                        const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
+                        xf = __fmul_ru(fmaf(dz, dz, fmaf(dy, dy, dx * dx)), 1.0f + 0x1p-21f);   // >= the exact d2
+                        cid = __float_as_int(c.w);
+                    } else {
+                        const int4 c = S.c[j];
+                        xf = __ll2float_ru(dist2<DIM>(L.q, c));
+                        cid = c.w;
+                    }
+                    if (!active || cid == L.q.id) xf = INFINITY;
+                    if (__any_sync(0xffffffffu, xf < L.fa[K - 1])) fa_insert<K>(L.fa, xf);
+                }
+            } else {
+                const float wb = L.wb;
+                const int64_t U = L.U;
+#pragma unroll 1
+                for (int j = 0; j < n32; ++j) {
+                    bool in;
+                    float xf;
+                    int32_t cid;
+                    if constexpr (DIM == 3) {
+                        const float4 c = S.f[j];
+                        const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
+                        const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                        in = df <= wb;
+                        xf = __fmul_ru(df, 1.0f + 0x1p-21f);
+                        cid = __float_as_int(c.w);
+                    } else {
+                        const int4 c = S.c[j];
+                        const int64_t d = dist2<DIM>(L.q, c);
+                        in = d <= U;
+                        xf = __ll2float_ru(d);
+                        cid = c.w;
+                    }
+                    if (in && cid != L.q.id) {
+                        if (L.cnt == Cap<DIM, K>::v) {   // rare (ties): keep the exact K best
+                            compact<DIM, K>(L, S, lane);
+                            if (L.cnt == Cap<DIM, K>::v) {
+                                mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
+                                compact<DIM, K>(L, S, lane);
+                            }
+                        }
+                        S.be[L.cnt][lane] = make_int2(b + j, __float_as_int(xf));
+                        ++L.cnt;
+                    }
+                }
+            }
+        }
+        if (pass == 0) {
+            if (active) set_bound<DIM, K>(L);
+        }
+    }
+}
+
+// Window seed (all-points queries): lane i first searches the 2*SeedW sorted positions
+// around its own (its Morton neighbours: Alg. 3's leaf seed, widened to a
+// fixed window so that every lane does the same amount of uniform work; queries are
+// walked in Morton order).  The window's records are staged once per packet in
+// shared memory (the idle stack); two passes as in seed_scan: fold every candidate into
+// fa, then buffer the candidates within the resulting bound.  The rest of the search
+// skips window positions on its hit path (each point is buffered at most once), so the
+// traversal covers the whole tree with the window's bound.
+template <int DIM, int K>
+__device__ __forceinline__ void window_seed(const int4* __restrict__ recs, int32_t n, int32_t p0, bool active,
+                                            Lane<DIM, K>& L, WarpSh<DIM, K>& S, int lane) {
+    static_assert(32 + 2 * kSeedW <= kStk, "the window is staged in the per-warp stack");
+    int4* W = S.stk;
+    const int32_t base = p0 - kSeedW;
+    __syncwarp();
+#pragma unroll
+    for (int t = lane; t < 32 + 2 * kSeedW; t += 32) {
+        const int32_t pos = base + t;
+        int4 v = make_int4(0, 0, 0, -1);   // outside [0, n): never a candidate
+        if (pos >= 0 && pos < n) {
+            v = __ldg(recs + pos);
+            if constexpr (DIM == 3)
+                v = make_int4(__float_as_int(__int2float_rn(v.x)), __float_as_int(__int2float_rn(v.y)),
+                              __float_as_int(__int2float_rn(v.z)), v.w);
+        }
+        W[t] = v;
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        const float wb = L.wb;
+        const int64_t U = L.U;
+#pragma unroll 4
+        for (int j = 0; j <= 2 * kSeedW; ++j) {
+            if (j == kSeedW) continue;   // the lane's own position (self)
+            const int4 c = W[lane + j];
+            float xf;
+            bool in;
+            if constexpr (DIM == 3) {
+                const float dx = L.qf[0] - __int_as_float(c.x), dy = L.qf[1] - __int_as_float(c.y),
+                            dz = L.qf[2] - __int_as_float(c.z);
+                const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+                xf = __fmul_ru(df, 1.0f + 0x1p-21f);   // >= the exact d2
+                in = df <= wb;
+            } else {
+                const int64_t d = dist2<DIM>(L.q, c);
+                xf = __ll2float_ru(d);
+                in = d <= U;
+            }
+            const bool valid = active && c.w >= 0;
+            if (pass == 0) {
+                if (!valid) xf = INFINITY;
+                if (__any_sync(0xffffffffu, xf < L.fa[K - 1])) fa_insert<K>(L.fa, xf);
+            } else if (valid && in) {
+                if (L.cnt == Cap<DIM, K>::v) {   // rare (ties): keep the exact K best
+                    compact<DIM, K>(L, S, lane);
+                    if (L.cnt == Cap<DIM, K>::v) {
+                        mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
+                        compact<DIM, K>(L, S, lane);
+                    }
+                }
+                S.be[L.cnt][lane] = make_int2(base + lane + j, __float_as_int(xf));
+                ++L.cnt;
+            }
+        }
+        if (pass == 0 && active) set_bound<DIM, K>(L);
+    }
+    __syncwarp();
 }
 
 // Scan the spans [s, mid) (lanes with needl) and [mid, e) (lanes with needr; mid == e
@@ -851,15 +1043,33 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
 #ifndef ZD_SEED_PAD
 #define ZD_SEED_PAD 1   // extra Morton-adjacent leaves scanned on each side of the seed
 #endif
-    int32_t sA = lA, sB = lB;
-    if (ZD_SEED_PAD > 0 && !A.root_based) {
-        const int32_t nleaves = __ldg(A.d_meta) + 1;
-        sA = max(0, lA - ZD_SEED_PAD);
-        sB = min(nleaves - 1, lB + ZD_SEED_PAD);
+#ifndef ZD_WSEED
+#define ZD_WSEED 1
+#endif
+    constexpr bool wseed = ZD_WSEED && !EXT;
+    int32_t ps_lo = 0, ps_hi = 0;   // sorted range scanned by the packet seed (skipped later)
+    L.wlo = INT32_MIN / 2;          // no window: the hit-path window test never fires
+#ifdef ZD_KNN_STATS
+    L.seed = true;
+#endif
+    if (A.root_based) {
+    } else if (wseed) {
+        L.wlo = p - kSeedW;
+        window_seed<DIM, K>(A.recs, A.n_pts, p0, active, L, S, lane);
+    } else {
+        int32_t sA = lA, sB = lB;
+        if (ZD_SEED_PAD > 0) {
+            const int32_t nleaves = __ldg(A.d_meta) + 1;
+            sA = max(0, lA - ZD_SEED_PAD);
+            sB = min(nleaves - 1, lB + ZD_SEED_PAD);
+        }
+        ps_lo = __ldg(A.leaf_start + sA);
+        ps_hi = __ldg(A.leaf_start + sB + 1);
+        seed_scan<DIM, K>(A.recs, ps_lo, ps_hi, active, L, S, lane);
     }
-    const int32_t ps_lo = A.root_based ? 0 : __ldg(A.leaf_start + sA);
-    const int32_t ps_hi = A.root_based ? 0 : __ldg(A.leaf_start + sB + 1);
-    if (!A.root_based) scan_span<DIM, K>(A.recs, ps_lo, ps_hi, active, L, S, lane);
+#ifdef ZD_KNN_STATS
+    L.seed = false;
+#endif
 
     if (can_defer && !A.root_based) {
         // A packet whose queries are far apart compared with their neighbour distances
@@ -916,6 +1126,10 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         P = -1;
     } else if (lA == lB) {
         P = __ldg(A.leaf_parent + lA);
+        if (wseed) {   // the window seed did not scan the packet's leaf as a whole
+            const int32_t ls = __ldg(A.leaf_start + lA), le = __ldg(A.leaf_start + lA + 1);
+            sub = Ref{~ls, ls, le};
+        }
     } else {
         // lowest common ancestor of leaves lA < lB = the separator node in [lA, lB)
         // with the highest split bit (the canonical tree is the Cartesian tree of the

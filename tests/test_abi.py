@@ -68,3 +68,16 @@ def test_product_does_not_import_oracle():
     for p in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")) + list(pkg.rglob("*.h")):
         text = p.read_text()
         assert "oracle" not in re.sub(r"#.*|//.*", "", text).lower().replace("oracle/ (the", ""), p
+
+
+def test_sort_key_limit_rejected_without_gpu(libpath):
+    """One radix sort holds < 2^30 keys (30-bit digit counts in the look-back words):
+    builds, insert batches and external query sets at or above it are refused before
+    any CUDA call."""
+    import paper_2111_04182_b200 as zd
+    lib = zd.load()
+    assert lib.zd_build_ex(None, 1 << 30, 3, None) is None
+    assert lib.zd_last_error_code() == zd.ZD_EINVAL
+    assert "2^30" in zd.last_error()
+    assert lib.zd_build_ex(None, (1 << 30) - 1, 3, None) is None   # NULL points: a different refusal
+    assert "NULL" in zd.last_error()

@@ -186,6 +186,27 @@ def test_insert_then_delete(zd, oracle_mod, dim):
     assert np.array_equal(r0[0], r1[0]) and np.array_equal(r0[1], r1[1])
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("n", [1, 2, 3, 9, 15, 16, 17])
+def test_insert_delete_tiny_trees(zd, oracle_mod, dim, n):
+    """Updates of trees that are a single leaf (2..16 points) or barely more: the
+    insert fast path must refuse them cleanly (the located leaf of a
+    single-leaf tree was left unwritten) and the result is the canonical tree."""
+    base = zdgen.uniform(n, dim, seed=900 + n)
+    t = zd.zd_build(dev(base))
+    live = oracle_mod.LiveSet(base)
+    for m, seed in ((1, 1), (2, 2), (5, 3)):
+        batch = zdgen.uniform(m, dim, seed=950 + 10 * n + seed)
+        assert t.zd_insert(dev(batch)) == live.insert(batch)
+        assert_same_structure(t.zd_export(), live.tree())
+        gi, gd = gpu_knn_all(t, 4)
+        oi, od, _ = live.tree().knn_all(4)
+        check_rows(gi, gd, oi, od)
+    kill = np.array([0, n + 1, n + 100], dtype=np.int32)
+    assert t.zd_delete(dev(kill)) == live.delete(kill)
+    assert_same_structure(t.zd_export(), live.tree())
+
+
 def test_delete_rows_and_live_ids(zd, oracle_mod):
     base = zdgen.uniform(40000, 3, seed=41)
     t = zd.zd_build(dev(base))
