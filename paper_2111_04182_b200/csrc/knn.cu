@@ -246,7 +246,10 @@ template <int DIM, int K>
 struct WarpSh {
     int4 c[DIM == 2 ? 32 : 1];           // 2D: staged candidates (x, y, 0, id)
 #if ZD_F32FILTER
-    float4 f[32];                        // 3D: the same in fp32 (exact below 2^24)
+    // 3D: the same in fp32 (exact below 2^24), structure of arrays so that one 16-byte
+    // load yields one axis of 4 candidates (packed f32x2 tests)
+    float fx[32], fy[32], fz[32];
+    int32_t fid[32];
 #endif
     int32_t p[32];                       // their sorted positions
     float4 pb[2 * kPG];                  // query box of each lane group (lo, hi; 2D: int bits)
@@ -256,6 +259,15 @@ struct WarpSh {
     int32_t dbg_npts, dbg_nint;          // bounds for ZD_DCHECK
 #endif
 };
+
+template <int DIM, int K>
+__device__ __forceinline__ float4 ldf(const WarpSh<DIM, K>& S, int j) {
+    return make_float4(S.fx[j], S.fy[j], S.fz[j], __int_as_float(S.fid[j]));
+}
+template <int DIM, int K>
+__device__ __forceinline__ void stf(WarpSh<DIM, K>& S, int j, float4 v) {
+    S.fx[j] = v.x; S.fy[j] = v.y; S.fz[j] = v.z; S.fid[j] = __float_as_int(v.w);
+}
 
 #ifndef ZD_SEEDW
 #define ZD_SEEDW 12      // window seed half-width (all-points queries)
@@ -490,7 +502,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
             if constexpr (DIM == 2) S.c[slot] = r;
             S.p[slot] = b + lane;
 #if ZD_F32FILTER
-            if (DIM == 3) S.f[slot] = fc;
+            if (DIM == 3) stf(S, slot, fc);
 #endif
         }
         __syncwarp();
@@ -517,18 +529,26 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 // in sub-blocks of ZD_SUB (uniform early exit: a short tail costs one
                 // sub-block, not a whole pass)
                 if constexpr (DIM == 3) {
+                    // 4 candidates per step: one 16-byte load per axis, packed f32x2
+                    // arithmetic in the same order as the scalar test (dx^2, + dy^2, + dz^2)
+                    static_assert(ZD_SUB3 == 4, "packed test handles 4 candidates per step");
                     const float wb = L.wb;
+                    const float2 qx = make_float2(L.qf[0], L.qf[0]), qy = make_float2(L.qf[1], L.qf[1]),
+                                 qz = make_float2(L.qf[2], L.qf[2]);
 #pragma unroll 1
-                    for (int j0 = 0; j0 < CH; j0 += ZD_SUB3) {
+                    for (int j0 = 0; j0 < CH; j0 += 4) {
                         if (j0 >= cnt) break;
-#pragma unroll
-                        for (int jj = 0; jj < ZD_SUB3; ++jj) {
-                            const int j = j0 + jj;
-                            const float4 c = S.f[h0 + j];
-                            const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
-                            const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-                            if (df <= wb) hit |= 1u << j;
-                        }
+                        const float4 X = *reinterpret_cast<const float4*>(&S.fx[h0 + j0]);
+                        const float4 Y = *reinterpret_cast<const float4*>(&S.fy[h0 + j0]);
+                        const float4 Z = *reinterpret_cast<const float4*>(&S.fz[h0 + j0]);
+                        const float2 dx0 = __fadd2_rn(qx, make_float2(-X.x, -X.y)), dx1 = __fadd2_rn(qx, make_float2(-X.z, -X.w));
+                        const float2 dy0 = __fadd2_rn(qy, make_float2(-Y.x, -Y.y)), dy1 = __fadd2_rn(qy, make_float2(-Y.z, -Y.w));
+                        const float2 dz0 = __fadd2_rn(qz, make_float2(-Z.x, -Z.y)), dz1 = __fadd2_rn(qz, make_float2(-Z.z, -Z.w));
+                        const float2 s0 = __ffma2_rn(dz0, dz0, __ffma2_rn(dy0, dy0, __fmul2_rn(dx0, dx0)));
+                        const float2 s1 = __ffma2_rn(dz1, dz1, __ffma2_rn(dy1, dy1, __fmul2_rn(dx1, dx1)));
+                        const uint32_t hb = (s0.x <= wb ? 1u : 0u) | (s0.y <= wb ? 2u : 0u) | (s1.x <= wb ? 4u : 0u) |
+                                            (s1.y <= wb ? 8u : 0u);
+                        hit |= hb << j0;
                     }
                 } else {
                     const int64_t U = L.U;
@@ -571,7 +591,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 const bool cv = lane < cnt;
                 uint32_t m = M;
                 if constexpr (DIM == 3) {
-                    const float4 c = S.f[h0 + (cv ? lane : 0)];
+                    const float4 c = ldf(S, h0 + (cv ? lane : 0));
                     while (m) {
                         const int i = __ffs(m) - 1;
                         m &= m - 1;
@@ -633,7 +653,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 float xf;
                 bool stale;   // outside the lane's current bound (it shrank since the test)
                 if constexpr (DIM == 3) {
-                    const float4 c = S.f[j];
+                    const float4 c = ldf(S, j);
                     const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
                     const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                     if (__float_as_int(c.w) == L.q.id) continue;   // self (excluded by id, reading 13)
@@ -690,7 +710,7 @@ __device__ __forceinline__ void seed_scan(const int4* __restrict__ recs, int32_t
             if (lane < n32) {
                 const int4 r = __ldg(recs + b + lane);
                 if constexpr (DIM == 3)
-                    S.f[lane] = make_float4(__int2float_rn(r.x), __int2float_rn(r.y), __int2float_rn(r.z), __int_as_float(r.w));
+                    stf(S, lane, make_float4(__int2float_rn(r.x), __int2float_rn(r.y), __int2float_rn(r.z), __int_as_float(r.w)));
                 else
                     S.c[lane] = r;
             }
@@ -701,7 +721,7 @@ __device__ __forceinline__ void seed_scan(const int4* __restrict__ recs, int32_t
                     float xf;
                     int32_t cid;
                     if constexpr (DIM == 3) {
-                        const float4 c = S.f[j];
+                        const float4 c = ldf(S, j);
                         const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
                         xf = __fmul_ru(fmaf(dz, dz, fmaf(dy, dy, dx * dx)), 1.0f + 0x1p-21f);   // >= the exact d2
                         cid = __float_as_int(c.w);
@@ -722,7 +742,7 @@ __device__ __forceinline__ void seed_scan(const int4* __restrict__ recs, int32_t
                     float xf;
                     int32_t cid;
                     if constexpr (DIM == 3) {
-                        const float4 c = S.f[j];
+                        const float4 c = ldf(S, j);
                         const float dx = L.qf[0] - c.x, dy = L.qf[1] - c.y, dz = L.qf[2] - c.z;
                         const float df = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
                         in = df <= wb;
