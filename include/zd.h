@@ -34,8 +34,10 @@
  *
  * Streams: all work runs on the handle's stream (zd_build_ex opts / zd_set_stream;
  * default: the legacy default stream).  zd_build, zd_insert and zd_delete
- * synchronize that stream once (to read a validation flag or a count).  zd_knn
- * with device outputs is asynchronous on the stream.
+ * synchronize that stream once (to read a validation flag, the tree's node count or
+ * the deleted count); only trees above 2^25 points, whose node buffers are sized
+ * from the node count, take one more sync per topology rebuild.  zd_knn with device
+ * outputs is asynchronous on the stream.
  *
  * Errors: functions returning int/int64 return a negative ZD_E* code on failure;
  * functions returning pointers return NULL.  zd_last_error() gives a
@@ -43,8 +45,12 @@
  * Validation happens before any mutation: a failed insert leaves the tree
  * unchanged (S:383 all-or-nothing).
  *
- * Concurrency: zd_knn may be called concurrently on one handle (read-only);
- * zd_insert / zd_delete / zd_set_stream / zd_free need exclusive access.
+ * Concurrency: zd_knn may be called concurrently on one handle from several host
+ * threads ("queries can be conducted in parallel"): it only reads the handle
+ * (the row map of the all-points output is refreshed by zd_insert / zd_delete),
+ * allocates its scratch per call and times itself with events of its own; device
+ * work of concurrent calls is ordered on the handle's stream.  zd_insert /
+ * zd_delete / zd_set_stream / zd_set_timing / zd_free need exclusive access.
  */
 #ifndef ZD_H
 #define ZD_H
@@ -93,7 +99,8 @@ typedef struct zd_opts {
 
 /* Build a zd-tree over n points (int32 [n][dim]); point i gets id i.
  * n = 0 is valid (single empty leaf).  Returns NULL on error: dim not in {2,3},
- * n < 0 or n >= 2^31 (ZD_EINVAL), a coordinate outside the box (ZD_ERANGE),
+ * n < 0 or n >= 2^30 (ZD_EINVAL: one radix sort holds < 2^30 keys), a coordinate
+ * outside the box (ZD_ERANGE),
  * allocation/CUDA failure.  Cite: Alg. 1 P:255-275. */
 ZD_API zd_tree *zd_build(const int32_t *points, int64_t n, int dim);
 ZD_API zd_tree *zd_build_ex(const int32_t *points, int64_t n, int dim, const zd_opts *opts);
@@ -144,8 +151,15 @@ ZD_API int zd_live_ids(const zd_tree *h, int32_t *out);
 /* Make all later work on h run on the given cudaStream_t (NULL = legacy default). */
 ZD_API int zd_set_stream(zd_tree *h, void *cuda_stream);
 
-/* Free the handle and all its device memory (NULL is a no-op). */
+/* Free the handle and all its device memory (NULL is a no-op).  The memory goes back
+ * to the library's private stream-ordered pool of the device (cached for the next
+ * build); zd_trim releases it. */
 ZD_API void zd_free(zd_tree *h);
+
+/* Release the memory cached in the library's pool on the current device back to the
+ * driver (cudaMemPoolTrimTo 0 after a device synchronize); live handles keep theirs.
+ * Returns ZD_OK or ZD_ECUDA. */
+ZD_API int zd_trim(void);
 
 /* Thread-local message for the last error on this thread ("" if none). */
 ZD_API const char *zd_last_error(void);

@@ -90,6 +90,8 @@ def load():
     L.zd_export.argtypes = [P, P, P, P, P, P]
     L.zd_set_timing.restype = i32
     L.zd_set_timing.argtypes = [P, i32]
+    L.zd_trim.restype = i32
+    L.zd_trim.argtypes = []
     L.zd_kernel_launches.restype = i64
     L.zd_kernel_launches.argtypes = []
     L.zd_get_timing.restype = i32
@@ -256,6 +258,11 @@ def zd_knn_stats(reset: bool = True) -> dict:
     return dict(zip(KNN_STATS[:n], out[:n].tolist()))
 
 
+def zd_trim() -> None:
+    """Release the memory cached in the library's device pool (zd_trim)."""
+    _check(load().zd_trim())
+
+
 def zd_kernel_launches() -> int:
     """Process-wide number of CUDA kernels libzd.so has launched."""
     return int(load().zd_kernel_launches())
@@ -279,5 +286,5 @@ def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None,
     return ZdTree(h, dim)
 
 
-__all__ = ["zd_build", "zd_kernel_launches", "zd_knn_stats", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "ZD_KNN_WARP", "PHASES",
+__all__ = ["zd_build", "zd_kernel_launches", "zd_trim", "zd_knn_stats", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "ZD_KNN_WARP", "PHASES",
            "ZD_OK", "ZD_EINVAL", "ZD_ERANGE", "ZD_ENOMEM", "ZD_ECUDA"]

@@ -1,9 +1,10 @@
 // api.cu — the C ABI of include/zd.h: handle, device memory, stream, orchestration.
 //
 // Host side only launches kernels (sort.cu, tree.cu, knn.cu, update.cu); every step
-// of the hot path runs on the GPU.  Memory comes from the device's stream-ordered
-// pool (cudaMallocAsync) with the release threshold raised, so repeated builds and
-// updates reuse memory without device-wide synchronisation.
+// of the hot path runs on the GPU.  Memory comes from a private stream-ordered pool per
+// device (cudaMallocFromPoolAsync) with the release threshold raised, so repeated
+// builds and updates reuse memory without device-wide synchronisation; zd_trim()
+// returns the cached memory.
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
@@ -22,6 +23,34 @@ using namespace zd;
 namespace zd {
 static std::atomic<int64_t> g_launches{0};
 void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+static PerDeviceOnce g_pool_once;
+static cudaMemPool_t g_pools[64] = {};
+
+static cudaMemPool_t device_pool() {
+    g_pool_once.run([](int dev) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t pool = nullptr;
+        if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            g_pools[dev & 63] = pool;
+        } else {
+            cudaGetLastError();   // fall back to the default pool
+        }
+    });
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return g_pools[dev & 63];
+}
+
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t st) {
+    cudaMemPool_t pool = device_pool();
+    return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+}
 }  // namespace zd
 
 namespace {
@@ -39,6 +68,15 @@ void clear_err() {
     g_err.clear();
     g_err_code = 0;
 }
+
+// Runs a cleanup at scope exit (scratch of an update that returns early on an error).
+template <class F>
+struct ScopeExit {
+    F f;
+    ~ScopeExit() { f(); }
+};
+template <class F>
+ScopeExit<F> at_exit(F f) { return ScopeExit<F>{f}; }
 
 int cuda_fail(cudaError_t e, const char* where) {
     cudaGetLastError();   // clear sticky-free errors
@@ -58,19 +96,6 @@ int cuda_fail(cudaError_t e, const char* where) {
         if (e_ != cudaSuccess) return cuda_fail(e_, where);        \
     } while (0)
 
-void pool_setup_once() {
-    static bool done = false;
-    if (done) return;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done = true;
-}
-
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a;
@@ -85,7 +110,7 @@ template <class T>
 cudaError_t dalloc(T** p, size_t count, cudaStream_t st) {
     *p = nullptr;
     if (count == 0) count = 1;
-    return cudaMallocAsync((void**)p, count * sizeof(T), st);
+    return pool_alloc((void**)p, count * sizeof(T), st);
 }
 
 template <class T>
@@ -163,11 +188,22 @@ struct zd_tree {
     bool host_meta_valid = false;
     int64_t n_leaves = 1, n_internal = 0;
     int32_t root = ~0;
+    std::mutex mu;   // guards ms[PH_KNN] written by concurrent zd_knn calls
+    // set while an update mutates the handle; left set if the update fails half-way
+    // (e.g. ENOMEM in the topology rebuild), after which every call refuses the handle
+    bool poisoned = false;
 };
 
 namespace {
 
 int* d_invalid(zd_tree* h) { return h->d_small + 4; }
+
+// NULL or poisoned handles are refused (ZD_EINVAL / ZD_ECUDA).
+int check_handle(const zd_tree* h) {
+    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    if (h->poisoned) return fail(ZD_ECUDA, "handle unusable: an earlier update failed half-way (free it)");
+    return ZD_OK;
+}
 unsigned long long* d_count(zd_tree* h) { return reinterpret_cast<unsigned long long*>(h->d_small + 6); }
 
 void free_tree_bufs(zd_tree* h) {
@@ -198,7 +234,7 @@ int alloc_node_bufs(zd_tree* h, int64_t ncap) {
     ZD_CUDA(dalloc(&t.visit, ncap, h->st));
     ZD_CUDA(dalloc(&t.range, 2 * ncap, h->st));
     ZD_CUDA(dalloc(&t.pos_range, ncap, h->st));
-    ZD_CUDA(cudaMallocAsync(&t.nodes, ncap * node_bytes, h->st));
+    ZD_CUDA(pool_alloc(&t.nodes, ncap * node_bytes, h->st));
     h->ncap = ncap;
     return ZD_OK;
 }
@@ -384,7 +420,7 @@ int stage_in(zd_tree* h, const void* src, size_t bytes, const void** dev, void**
     *owned = nullptr;
     if (bytes == 0 || is_device_ptr(src)) { *dev = src; return ZD_OK; }
     void* d = nullptr;
-    ZD_CUDA(cudaMallocAsync(&d, bytes, h->st));
+    ZD_CUDA(pool_alloc(&d, bytes, h->st));
     ZD_CUDA(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, h->st));
     *owned = d;
     *dev = d;
@@ -404,7 +440,6 @@ void destroy(zd_tree* h) {
 }
 
 int do_build(zd_tree* h, const int32_t* points, int64_t n) {
-    pool_setup_once();
     ZD_CUDA(dalloc(&h->d_small, 8, h->st));
     h->h_small = pinned().get();
     if (!h->h_small) h->h_small = new int32_t[8];
@@ -504,6 +539,15 @@ int zd_set_timing(zd_tree* h, int enable) {
 
 int64_t zd_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
+int zd_trim(void) {
+    clear_err();
+    cudaMemPool_t pool = device_pool();
+    if (!pool) return ZD_OK;
+    ZD_CUDA(cudaDeviceSynchronize());   // frees still pending on streams complete first
+    ZD_CUDA(cudaMemPoolTrimTo(pool, 0));
+    return ZD_OK;
+}
+
 int zd_knn_stats(int64_t* out, int n, int reset) {
     clear_err();
     if (!out || n < 0) return fail(ZD_EINVAL, "zd_knn_stats: bad arguments");
@@ -526,7 +570,7 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
 int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_idx, int64_t* out_dist2, int flags) {
     clear_err();
     if (flags & ~(ZD_KNN_ROOT_BASED | ZD_KNN_WARP)) return fail(ZD_EINVAL, "zd_knn_ex: unknown flags");
-    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    if (int e = check_handle(h)) return e;
     if (k < 1 || k > ZD_K_MAX) return fail(ZD_EINVAL, "zd_knn: k must be in [1, ZD_K_MAX]");
     if (m < 0 || (queries ? m >= kMaxSortKeys : m >= ((int64_t)1 << 31) - 1))
         return fail(ZD_EINVAL, "zd_knn: bad m (external queries: m < 2^30)");
@@ -568,13 +612,19 @@ int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out
     a.split_bit = h->tb.split_bit;
     a.d_meta = h->d_small;
     a.out_idx = di; a.out_d2 = dd;
+    // zd_knn only reads the handle (concurrent calls are allowed): the row map is
+    // refreshed by the mutators, timing uses events of this call
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (h->timing) {
+        ZD_CUDA(cudaEventCreate(&ev0));
+        ZD_CUDA(cudaEventCreate(&ev1));
+    }
     if (!queries) {
-        if ((rc = ensure_rows(h))) return rc;
         a.row_of_id = h->rows_identity ? nullptr : h->row_of_id;
-        rec(h, 0);
+        if (ev0) cudaEventRecord(ev0, h->st);
         knn_all(a, h->st);
         ZD_CHECK_LAUNCH("knn_all");
-        rec(h, 1);
+        if (ev1) cudaEventRecord(ev1, h->st);
     } else {
         const void* dq = nullptr;
         void* owned = nullptr;
@@ -597,11 +647,11 @@ int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out
         ZD_CUDA(dalloc(&qk, m, h->st));
         ZD_CUDA(dalloc(&qr, m, h->st));
         ZD_CUDA(dalloc(&ql, m, h->st));
-        rec(h, 0);
+        if (ev0) cudaEventRecord(ev0, h->st);
         if ((rc = sort_into(h, (const int32_t*)dq, m, 0, qk, qr))) return rc;
         knn_queries(a, qk, qr, ql, m, h->st);
         ZD_CHECK_LAUNCH("knn_queries");
-        rec(h, 1);
+        if (ev1) cudaEventRecord(ev1, h->st);
         if (owned) cudaFreeAsync(owned, h->st);
         dfree(qk, h->st);
         dfree(qr, h->st);
@@ -615,16 +665,22 @@ int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out
         dfree(dd, h->st);
         ZD_CUDA(cudaStreamSynchronize(h->st));
     }
-    if (h->timing) {
-        ZD_CUDA(cudaEventSynchronize(h->ev[1]));
-        elapsed(h, PH_KNN, 0, 1);
+    if (ev0) {
+        float t = 0.f;
+        ZD_CUDA(cudaEventSynchronize(ev1));
+        if (cudaEventElapsedTime(&t, ev0, ev1) == cudaSuccess) {
+            std::lock_guard<std::mutex> g(h->mu);
+            h->ms[PH_KNN] = t;
+        }
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
     }
     return ZD_OK;
 }
 
 int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     clear_err();
-    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    if (int e = check_handle(h)) return e;
     if (m < 0 || m >= kMaxSortKeys) return fail(ZD_EINVAL, "zd_insert: need 0 <= m < 2^30");
     if (m == 0) return h->n_next;
     if (!batch) return fail(ZD_EINVAL, "zd_insert: batch is NULL");
@@ -633,43 +689,53 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     const void* db = nullptr;
     void* owned = nullptr;
     if ((rc = stage_in(h, batch, (size_t)m * h->dim * sizeof(int32_t), &db, &owned))) return rc;
-    // validation before any mutation
+    // validation before any mutation; the batch is sorted into scratch and the
+    // fast-path check runs before the one sync, which reads the validation flag, the
+    // check's verdict and the node meta together
     rec(h, 0);
     ZD_CUDA(cudaMemsetAsync(d_invalid(h), 0, 2 * sizeof(int), h->st));   // [4] invalid, [5] fast path refused
     validate_points(h->dim, (const int32_t*)db, m, d_invalid(h), h->st);
-    ZD_CUDA(cudaMemcpyAsync(h->h_small + 4, d_invalid(h), sizeof(int), cudaMemcpyDeviceToHost, h->st));
     rec(h, 1);
-    ZD_CUDA(cudaStreamSynchronize(h->st));
-    if (h->h_small[4]) {
-        if (owned) cudaFreeAsync(owned, h->st);
-        return fail(ZD_ERANGE, "zd_insert: coordinate outside the universe box (tree unchanged)");
-    }
     const int64_t first = h->n_next;
     // sorted batch with ids first.. (K7)
     uint64_t* bk = nullptr;
     int4* br = nullptr;
+    int32_t* bleaf = nullptr;
+    auto free_scratch = [&]() {
+        dfree(bk, h->st);
+        dfree(br, h->st);
+        dfree(bleaf, h->st);
+        if (owned) cudaFreeAsync(owned, h->st);
+        owned = nullptr;
+    };
+    auto scratch_guard = at_exit(free_scratch);
     ZD_CUDA(dalloc(&bk, m, h->st));
     ZD_CUDA(dalloc(&br, m, h->st));
     rec(h, 2);
     if ((rc = sort_into(h, (const int32_t*)db, m, (uint32_t)first, bk, br))) return rc;
-    if (owned) cudaFreeAsync(owned, h->st);
     // NEXT-2 fast path (incr.cu): a small batch that keeps the canonical topology is
-    // applied by position shifts and a box refit instead of the full rebuild (its
-    // check costs one more sync, so only small batches try it)
-    int32_t* bleaf = nullptr;
-    bool try_fast = incr_enabled() && h->n > 1 && m <= kIncrMaxBatch;
-    if (try_fast && (rc = refresh_host_meta(h))) return rc;   // valid after a build: no sync
-    try_fast = try_fast && h->root >= 0;                     // a single-leaf tree rebuilds
+    // applied by position shifts and a box refit instead of the full rebuild (a
+    // single-leaf tree is refused by the check itself)
+    const bool try_fast = incr_enabled() && h->n > 1 && m <= kIncrMaxBatch;
     if (try_fast) {
         ZD_CUDA(dalloc(&bleaf, m, h->st));
         KnnArgs t{};
         t.nodes = h->tb.nodes; t.split_bit = h->tb.split_bit; t.d_meta = h->d_small; t.leaf_start = h->tb.leaf_start;
         incr_locate(h->dim, bk, m, t, h->keys, h->leaf_max, bleaf, d_invalid(h) + 1, h->st);
         ZD_CHECK_LAUNCH("incr_locate");
-        ZD_CUDA(cudaMemcpyAsync(h->h_small + 5, d_invalid(h) + 1, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-        ZD_CUDA(cudaStreamSynchronize(h->st));
     }
+    ZD_CUDA(cudaMemcpyAsync(h->h_small, h->d_small, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
+    ZD_CUDA(cudaStreamSynchronize(h->st));   // the one sync
+    if (h->h_small[4]) {
+        free_scratch();
+        return fail(ZD_ERANGE, "zd_insert: coordinate outside the universe box (tree unchanged)");
+    }
+    h->n_internal = h->h_small[0];
+    h->n_leaves = h->n_internal + 1;
+    h->root = h->h_small[1];
+    h->host_meta_valid = true;
     const bool fast = try_fast && !h->h_small[5];
+    h->poisoned = true;   // cleared when the update completes
     rec(h, 3);
     // growth hands back the old primary arrays as the merge source (no copy)
     uint64_t* src_k = h->keys;
@@ -687,19 +753,17 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     dfree(old_k, h->st);
     dfree(old_r, h->st);
     if (fast) {
-        if ((rc = refresh_host_meta(h))) return rc;   // no-op when valid (it is after a build)
         incr_apply(h->dim, h->n_internal, bleaf, br, m, h->tb.leaf_start, h->tb.pt_leaf, h->tb.nodes, h->tb.range,
                    h->tb.pos_range, h->tb.leaf_parent, h->st);
         ZD_CHECK_LAUNCH("incr_apply");
         h->fast_inserts += 1;
     }
-    dfree(bk, h->st);
-    dfree(br, h->st);
-    dfree(bleaf, h->st);
+    free_scratch();
     set_alive_range(h->alive, first, m, h->st);
     h->n += m;
     h->n_next += m;
     if (!h->rows_identity) h->rows_dirty = true;
+    if ((rc = ensure_rows(h))) return rc;   // zd_knn reads the row map without refreshing it
     rec(h, 4);
     if (fast) {
         if (h->timing) ZD_CUDA(cudaEventRecord(h->ev[6], h->st));   // no topology / box phase
@@ -707,6 +771,7 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
         return rc;
     }
     rec(h, 5);
+    h->poisoned = false;
     if (h->timing) {
         ZD_CUDA(cudaEventSynchronize(h->ev[5]));
         elapsed(h, PH_VALID, 0, 1);
@@ -720,7 +785,7 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
 
 int64_t zd_delete(zd_tree* h, const int32_t* ids, int64_t m) {
     clear_err();
-    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    if (int e = check_handle(h)) return e;
     if (m < 0) return fail(ZD_EINVAL, "zd_delete: m < 0");
     if (m == 0 || h->n == 0) return 0;
     if (!ids) return fail(ZD_EINVAL, "zd_delete: ids is NULL");
@@ -734,43 +799,43 @@ int64_t zd_delete(zd_tree* h, const int32_t* ids, int64_t m) {
     compact_alive(h->alive, h->keys, h->recs, h->n, h->keys2, h->recs2, h->tb.block_cnt, h->st);
     ZD_CHECK_LAUNCH("delete");
     if (owned) cudaFreeAsync(owned, h->st);
-    // NEXT-2 delete fast path (incr.cu): checked before the count readback's sync
+    // NEXT-2 delete fast path (incr.cu): checked on the device before the one sync,
+    // which reads the deleted count, the check's verdict and the node meta together
     int32_t* del_before = nullptr;
     uint32_t* dscratch = nullptr;
-    bool try_fast = incr_enabled() && m <= kIncrMaxBatch && h->n > 1;
-    if (try_fast && (rc = refresh_host_meta(h))) return rc;   // a sync only after a full rebuild
-    try_fast = try_fast && h->root >= 0;
+    auto scratch_guard = at_exit([&]() { dfree(del_before, h->st); dfree(dscratch, h->st); });
+    const bool try_fast = incr_enabled() && m <= kIncrMaxBatch && h->n > 1;
+    const int64_t ncap = h->ncap, nblk_cap = (ncap + 1 + 255) / 256;
     if (try_fast) {
-        const int64_t nb = h->n_internal, nl = nb + 1;
-        const int64_t nblk = (nl + 255) / 256;
-        ZD_CUDA(dalloc(&del_before, nl + 1, h->st));
-        ZD_CUDA(dalloc(&dscratch, 2 * nb + nblk + 2, h->st));   // mark [nb] | arrived [nb] | bsum [nblk+1]
-        ZD_CUDA(cudaMemsetAsync(dscratch, 0, 2 * nb * sizeof(uint32_t), h->st));
+        ZD_CUDA(dalloc(&del_before, ncap + 2, h->st));
+        ZD_CUDA(dalloc(&dscratch, 2 * ncap + nblk_cap + 2, h->st));   // mark [ncap] | arrived [ncap] | bsum
         ZD_CUDA(cudaMemsetAsync(d_invalid(h) + 1, 0, sizeof(int), h->st));
-        decr_check(nb, h->recs, h->tb.leaf_start, h->alive, h->tb.range, h->leaf_max, del_before, dscratch + 2 * nb,
-                   d_invalid(h) + 1, h->st);
+        decr_check(ncap, h->d_small, h->recs, h->tb.leaf_start, h->alive, h->tb.range, h->leaf_max, del_before,
+                   dscratch + 2 * ncap, d_invalid(h) + 1, h->st);
         ZD_CHECK_LAUNCH("decr_check");
-        ZD_CUDA(cudaMemcpyAsync(h->h_small + 5, d_invalid(h) + 1, sizeof(int), cudaMemcpyDeviceToHost, h->st));
     }
-    ZD_CUDA(cudaMemcpyAsync(h->h_small + 6, d_count(h), sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->st));
+    ZD_CUDA(cudaMemcpyAsync(h->h_small, h->d_small, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
     rec(h, 1);
-    ZD_CUDA(cudaStreamSynchronize(h->st));
+    ZD_CUDA(cudaStreamSynchronize(h->st));   // the one sync
+    h->n_internal = h->h_small[0];
+    h->n_leaves = h->n_internal + 1;
+    h->root = h->h_small[1];
+    h->host_meta_valid = true;
     unsigned long long cnt;
     std::memcpy(&cnt, h->h_small + 6, sizeof(cnt));
-    if (cnt == 0) {
-        dfree(del_before, h->st);
-        dfree(dscratch, h->st);
-        return 0;
-    }
+    if (cnt == 0) return 0;
     const bool fast = try_fast && !h->h_small[5];
+    h->poisoned = true;   // cleared when the update completes
     std::swap(h->keys, h->keys2);
     std::swap(h->recs, h->recs2);
     h->n -= (int64_t)cnt;
     h->rows_identity = false;
     h->rows_dirty = true;
+    if ((rc = ensure_rows(h))) return rc;   // zd_knn reads the row map without refreshing it
     rec(h, 2);
     if (fast) {
         const int64_t nb = h->n_internal;
+        ZD_CUDA(cudaMemsetAsync(dscratch, 0, 2 * nb * sizeof(uint32_t), h->st));   // mark | arrived
         decr_apply(h->dim, nb, del_before, h->tb.leaf_start, h->tb.pt_leaf, h->tb.nodes, h->tb.range, h->tb.pos_range,
                    h->tb.leaf_parent, h->recs, dscratch, dscratch + nb, h->st);
         ZD_CHECK_LAUNCH("decr_apply");
@@ -779,9 +844,8 @@ int64_t zd_delete(zd_tree* h, const int32_t* ids, int64_t m) {
     } else if ((rc = topology(h))) {
         return rc;
     }
-    dfree(del_before, h->st);
-    dfree(dscratch, h->st);
     rec(h, 3);
+    h->poisoned = false;
     if (h->timing) {
         ZD_CUDA(cudaEventSynchronize(h->ev[3]));
         elapsed(h, PH_MERGE, 0, 1);
@@ -794,7 +858,8 @@ int64_t zd_delete(zd_tree* h, const int32_t* ids, int64_t m) {
 int zd_live_ids(const zd_tree* hc, int32_t* out) {
     clear_err();
     zd_tree* h = const_cast<zd_tree*>(hc);
-    if (!h || (!out && h->n > 0)) return fail(ZD_EINVAL, "NULL argument");
+    if (int e = check_handle(h)) return e;
+    if (!out && h->n > 0) return fail(ZD_EINVAL, "NULL argument");
     if (h->n == 0) return ZD_OK;
     int rc;
     if (h->rows_identity) {
@@ -831,7 +896,7 @@ int zd_get_info(const zd_tree* hc, zd_info* out) {
 int zd_export(const zd_tree* hc, uint64_t* keys, int32_t* recs, int32_t* leaf_start, int32_t* leaf_parent,
               int32_t* nodes) {
     zd_tree* h = const_cast<zd_tree*>(hc);
-    if (!h) return fail(ZD_EINVAL, "NULL handle");
+    if (int e = check_handle(h)) return e;
     int rc = refresh_host_meta(h);
     if (rc) return rc;
     const cudaMemcpyKind K = cudaMemcpyDefault;
@@ -842,7 +907,7 @@ int zd_export(const zd_tree* hc, uint64_t* keys, int32_t* recs, int32_t* leaf_st
     if (nodes && h->n_internal) {
         const size_t bytes = (size_t)h->n_internal * (4 * h->dim + 4) * sizeof(int32_t);
         int32_t* tmp = nullptr;
-        ZD_CUDA(cudaMallocAsync((void**)&tmp, bytes, h->st));
+        ZD_CUDA(pool_alloc((void**)&tmp, bytes, h->st));
         export_nodes(h->dim, h->tb.nodes, h->tb.split_bit, h->n_internal, tmp, h->st);
         ZD_CHECK_LAUNCH("export_nodes");
         ZD_CUDA(cudaMemcpyAsync(nodes, tmp, bytes, K, h->st));

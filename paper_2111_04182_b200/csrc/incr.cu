@@ -171,13 +171,19 @@ __global__ void __launch_bounds__(256) incr_refit_kernel(Node<DIM>* __restrict__
 // last dirty child arrives).
 
 // per leaf: dead records (old positions, alive bitset by id), emptied-leaf check,
-// block-exclusive scan into del_before, block totals into bsum
+// block-exclusive scan into del_before, block totals into bsum.  The grid covers the
+// node capacity; the live leaf count comes from the device meta (meta[0] internal
+// nodes, meta[1] root: a single-leaf tree takes the full rebuild), so the host needs no
+// node count before the launch.
 __global__ void __launch_bounds__(256) decr_count_kernel(const int4* __restrict__ recs,
-                                                         const int32_t* __restrict__ leaf_start, int32_t nleaves,
+                                                         const int32_t* __restrict__ leaf_start,
+                                                         const int32_t* __restrict__ meta,
                                                          const uint32_t* __restrict__ alive, int32_t* __restrict__ del_before,
                                                          uint32_t* __restrict__ bsum, int* __restrict__ bad) {
     __shared__ uint32_t s_warp[32];
+    const int32_t nleaves = __ldg(meta) + 1;
     const int32_t l = blockIdx.x * 256 + threadIdx.x;
+    if (l == 0 && __ldg(meta + 1) < 0) atomicOr(bad, 1);
     uint32_t c = 0;
     if (l < nleaves) {
         const int32_t s = __ldg(leaf_start + l), e = __ldg(leaf_start + l + 1);
@@ -194,20 +200,21 @@ __global__ void __launch_bounds__(256) decr_count_kernel(const int4* __restrict_
 }
 
 // del_before[l] += block offset; del_before[nleaves] = total
-__global__ void __launch_bounds__(256) decr_fix_kernel(int32_t* __restrict__ del_before, int32_t nleaves,
+__global__ void __launch_bounds__(256) decr_fix_kernel(int32_t* __restrict__ del_before, const int32_t* __restrict__ meta,
                                                        const uint32_t* __restrict__ bsum, uint32_t nblocks) {
+    const int32_t nleaves = __ldg(meta) + 1;
     const int32_t l = blockIdx.x * 256 + threadIdx.x;
     if (l < nleaves) del_before[l] += (int32_t)__ldg(bsum + (l >> 8));
     else if (l == nleaves) del_before[l] = (int32_t)__ldg(bsum + nblocks);
 }
 
 // every internal node keeps > leaf_max points
-__global__ void __launch_bounds__(256) decr_check_kernel(int32_t nb, const int32_t* __restrict__ range,
+__global__ void __launch_bounds__(256) decr_check_kernel(const int32_t* __restrict__ meta, const int32_t* __restrict__ range,
                                                          const int32_t* __restrict__ leaf_start,
                                                          const int32_t* __restrict__ del_before, int leaf_max,
                                                          int* __restrict__ bad) {
     const int32_t i = blockIdx.x * 256 + threadIdx.x;
-    if (i >= nb) return;
+    if (i >= __ldg(meta)) return;
     const int32_t L = __ldg(range + 2 * i), R = __ldg(range + 2 * i + 1);
     const int32_t size = __ldg(leaf_start + R + 1) - __ldg(leaf_start + L);
     const int32_t del = __ldg(del_before + R + 1) - __ldg(del_before + L);
@@ -326,15 +333,17 @@ void incr_apply(int dim, int64_t nb, const int32_t* bleaf, const int4* brecs, in
 
 namespace zd {
 
-int decr_check(int64_t nb, const int4* recs_old, const int32_t* leaf_start, const uint32_t* alive,
-               const int32_t* range, int leaf_max, int32_t* del_before, uint32_t* bsum, int* bad, cudaStream_t st) {
-    const int32_t nleaves = (int32_t)nb + 1;
-    const uint32_t nblk = (uint32_t)((nleaves + 255) / 256);
+int decr_check(int64_t nb_cap, const int32_t* meta, const int4* recs_old, const int32_t* leaf_start,
+               const uint32_t* alive, const int32_t* range, int leaf_max, int32_t* del_before, uint32_t* bsum, int* bad,
+               cudaStream_t st) {
+    const int64_t nl_cap = nb_cap + 1;
+    const uint32_t nblk = (uint32_t)((nl_cap + 255) / 256);
     count_launch(4);
-    decr_count_kernel<<<nblk, 256, 0, st>>>(recs_old, leaf_start, nleaves, alive, del_before, bsum, bad);
+    decr_count_kernel<<<nblk, 256, 0, st>>>(recs_old, leaf_start, meta, alive, del_before, bsum, bad);
     scan_blocks_kernel<<<1, 1024, 0, st>>>(bsum, nblk);
-    decr_fix_kernel<<<(nleaves + 1 + 255) / 256, 256, 0, st>>>(del_before, nleaves, bsum, nblk);
-    if (nb > 0) decr_check_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>((int32_t)nb, range, leaf_start, del_before, leaf_max, bad);
+    decr_fix_kernel<<<(unsigned)((nl_cap + 1 + 255) / 256), 256, 0, st>>>(del_before, meta, bsum, nblk);
+    if (nb_cap > 0)
+        decr_check_kernel<<<(unsigned)((nb_cap + 255) / 256), 256, 0, st>>>(meta, range, leaf_start, del_before, leaf_max, bad);
     return 0;
 }
 

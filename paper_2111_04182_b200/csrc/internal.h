@@ -1,11 +1,36 @@
 // internal.h — host-side launch interface between the CUDA translation units.
 #pragma once
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace zd {
+
+// One-time setup per CUDA device (devices 0..63), safe under concurrent callers: the
+// per-device flag is published with release order after f() ran, under a mutex.
+struct PerDeviceOnce {
+    std::atomic<uint64_t> done{0};
+    std::mutex mu;
+    template <class F>
+    void run(F&& f) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t bit = 1ull << (dev & 63);
+        if (done.load(std::memory_order_acquire) & bit) return;
+        std::lock_guard<std::mutex> g(mu);
+        if (done.load(std::memory_order_relaxed) & bit) return;
+        f(dev);
+        done.fetch_or(bit, std::memory_order_release);
+    }
+};
+
+// Stream-ordered allocations come from a private memory pool per device (not the
+// device's default pool, which other code in the process may use), with the release
+// threshold raised so repeated builds reuse memory; zd_trim() hands it back.
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t st);
 
 // process-wide count of kernel launches issued by this library (zd_kernel_launches)
 void count_launch(int k = 1);
@@ -92,11 +117,14 @@ void incr_apply(int dim, int64_t nb, const int32_t* bleaf, const int4* brecs, in
                 int32_t* pt_leaf, void* nodes, const int32_t* range, int2* pos_range, const int32_t* leaf_parent,
                 cudaStream_t st);
 // Delete fast path: dead records per leaf (old arrays + alive bitset) scanned into
-// del_before [nleaves+1] (bsum: block scratch), *bad if a leaf empties or an internal
-// node drops to <= leaf_max points; then the position shifts and dirty-path box refit
-// (mark, arrived: zeroed node-sized scratch).
-int decr_check(int64_t nb, const int4* recs_old, const int32_t* leaf_start, const uint32_t* alive,
-               const int32_t* range, int leaf_max, int32_t* del_before, uint32_t* bsum, int* bad, cudaStream_t st);
+// del_before [nleaves+1] (bsum: block scratch), *bad if a leaf empties, an internal
+// node drops to <= leaf_max points or the tree is a single leaf; then the position
+// shifts and dirty-path box refit (mark, arrived: zeroed node-sized scratch).  The
+// check is launched over the node capacity nb_cap and reads the node count from the
+// device meta (meta[0] internal nodes, meta[1] root): no host sync before it.
+int decr_check(int64_t nb_cap, const int32_t* meta, const int4* recs_old, const int32_t* leaf_start,
+               const uint32_t* alive, const int32_t* range, int leaf_max, int32_t* del_before, uint32_t* bsum, int* bad,
+               cudaStream_t st);
 void decr_apply(int dim, int64_t nb, const int32_t* del_before, int32_t* leaf_start, int32_t* pt_leaf, void* nodes,
                 const int32_t* range, int2* pos_range, const int32_t* leaf_parent, const int4* recs_new, uint32_t* mark,
                 uint32_t* arrived, cudaStream_t st);

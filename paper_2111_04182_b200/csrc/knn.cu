@@ -1330,11 +1330,10 @@ void launch_packets(const PacketArgs& A, cudaStream_t st) {
     const int grid = (int)((warps + Pw<K>::v - 1) / Pw<K>::v);
     if (grid <= 0) return;
     const size_t smem = sizeof(WarpSh<DIM, K>) * Pw<K>::v;
-    static bool attr_set = false;   // per template instance
-    if (!attr_set) {
+    static PerDeviceOnce attr;   // per template instance and device (concurrent zd_knn calls)
+    attr.run([&](int) {
         cudaFuncSetAttribute(knn_packet_kernel<DIM, K, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
+    });
     count_launch(1);
     knn_packet_kernel<DIM, K, EXT><<<grid, Pw<K>::v * 32, smem, st>>>(A);
     if (A.hard_list) {

@@ -689,3 +689,51 @@ def test_delete_fast_path(zd, oracle_mod, monkeypatch, dist, dim):
     gi, gd = gpu_knn_all(t, 10)
     oi, od, _ = live.tree().knn_all(10)
     check_rows(gi, gd, oi, od)
+
+
+def test_concurrent_knn_one_handle(zd, oracle_mod):
+    """zd_knn is re-entrant on one handle ("queries can be conducted in
+    parallel"): two host threads query the same tree, after updates (row map) and with
+    timing on (per-call events), and both get the oracle's rows."""
+    import threading
+    base = zdgen.uniform(30000, 3, seed=61)
+    t = zd.zd_build(dev(base))
+    live = oracle_mod.LiveSet(base)
+    batch = zdgen.uniform(3000, 3, seed=62)
+    t.zd_insert(dev(batch)); live.insert(batch)
+    kill = zdgen.delete_ids(30000, 2000, seed=63)
+    t.zd_delete(dev(kill)); live.delete(kill)
+    t.zd_set_timing(True)
+    oi, od, _ = live.tree().knn_all(10)
+    qs = zdgen.uniform(5000, 3, seed=64)
+    qi, qd, _ = live.tree().knn_queries(qs, 5)
+    errors = []
+
+    def worker(external):
+        try:
+            for _ in range(6):
+                if external:
+                    gi, gd = t.zd_knn(5, queries=dev(qs))
+                    torch.cuda.synchronize()
+                    check_rows(gi.cpu().numpy(), gd.cpu().numpy(), qi, qd)
+                else:
+                    gi, gd = gpu_knn_all(t, 10)
+                    check_rows(gi, gd, oi, od)
+        except Exception as e:  # noqa: BLE001 - reported below
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(x,)) for x in (False, True, False)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors[0]
+    assert t.zd_get_timing()["knn"] > 0
+
+
+def test_trim_releases_pool(zd):
+    t = zd.zd_build(dev(zdgen.uniform(200000, 3, seed=65)))
+    t.zd_free()
+    assert zd.load().zd_trim() == 0
+    t = zd.zd_build(dev(zdgen.uniform(1000, 3, seed=66)))   # the pool grows again on demand
+    assert t.zd_size() == 1000
