@@ -11,8 +11,15 @@ are reported beside it.
 Timing: inputs resident in HBM; W untimed warm-up steps; K timed steps, each
 bracketed by CUDA events on the working stream with a 256 MB L2 flush (> 126 MB L2)
 between steps outside the timed region; barrier + synchronize around the timed
-loop; max over ranks.  Multi-GPU: replicas only — every rank runs its own
-full step on its own GPU, value = all ranks' queries / max time ("weak").
+loop; max over ranks.  Multi-GPU (the parallel-for over queries
+of P:53 / P:543): every rank holds a replica of the tree (it runs the build and both
+updates itself: no exchange) and answers one contiguous Morton range of the 10^7
+queries (zd_knn_range); value = the 10^7 queries / max time over ranks ("strong").
+
+Beside the headline (rank 0, one GPU): a per-config report for C1-C4b (build and
+k-NN throughput with their roofline fractions, every row compared with the oracle),
+the oracle timed on the host cores at full size (all cores; one thread for C1 and a
+10^6-point C3 sample) and the CPU model.
 
 --impl reference: the CPU oracle (oracle/, the only other place bench.py executes
 it) on the host cores, on a bounded sample of the same workload.
@@ -175,7 +182,7 @@ def config_block(extra=None):
          "n": c["n"], "dim": c["dim"], "k": K_NN, "insert_m": c["insert_m"], "delete_m": c["delete_m"],
          "leaf_max": 16, "seeds": {"base": c["seed"], "insert": c["insert_seed"], "delete": c["delete_seed"]},
          "l2": "flushed between timed steps (256 MB write, outside the timed region)",
-         "parallelism": "replicas"}
+         "parallelism": "query shards (contiguous Morton ranges), tree replicated per GPU"}
     if extra:
         d.update(extra)
     return d
@@ -203,10 +210,12 @@ def cpu_baseline(sample_n: int):
     pts, batch, kill = workload_inputs(sample_n)
     dt, nq, cnt = oracle_step(pts, batch, kill)
     per_q = {k: v / nq for k, v in cnt.items()}
+    full = sample_n == zdgen.CONFIGS[WORKLOAD]["n"]
+    what = "one full C5 step" if full else f"one C5 step scaled to n={sample_n:,}"
     return {"value": nq / dt, "unit": UNIT, "cores": oracle.num_cores(), "kind": "oracle",
-            "sample": f"one full C5 step scaled to n={sample_n:,} (insert {len(batch):,}, delete {len(kill):,}): "
-                      f"3 sequential oracle builds + leaf-based k=10 query on all cores",
-            "seconds": dt}, per_q
+            "sample": f"{what} (insert {len(batch):,}, delete {len(kill):,}): 3 sequential oracle builds + "
+                      f"leaf-based k=10 query of the {nq:,} live points on all cores",
+            "seconds": dt, "cpu_model": cpu_model()}, per_q
 
 
 def run_reference(args, D: Dist):
@@ -227,25 +236,80 @@ def run_reference(args, D: Dist):
               f"on the host cores")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": config_block({"reference_sample_n": n}),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_cores(), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------- GPU leg
 
-# Algorithmic integer work per query, in int32-lane operations:
-# distance eval 3D = 3 sub + 3 mul + 2 add + 1 compare = 9; box distance = 7/axis + 1 = 22;
-# k-best replacement = 3K (K compares + 2K selects) = 30; ascent stop test = 4/axis + 3 = 15.
-OPS_DIST, OPS_BOX, OPS_REPL, OPS_ASCENT = 9, 22, 3 * K_NN, 15
+# Algorithmic work per query, in lane-instructions: the oracle's counters (the paper's
+# Alg. 3 + Alg. 2 on the same input) times the SASS cost of each operation as the k-NN
+# kernel implements it (scripts/op_costs.py -> profiles/r02_op_costs.json: distance
+# test per candidate, box test per child box, k-best insertion, ascent stop test).
+# Fallback (no file): the survey's hand estimates 9 / 22 / 30 / 15.
+def _op_costs():
+    try:
+        d = json.loads((ROOT / "profiles" / "r02_op_costs.json").read_text())["ops"]
+        return ({k: d[k]["lane_instructions"] for k in ("dist", "box", "insert", "ascent")},
+                {k: d[k]["half_rate_instructions"] for k in ("dist", "box", "insert", "ascent")},
+                "profiles/r02_op_costs.json (cuobjdump -sass of scripts/op_costs.cu)")
+    except Exception:
+        return (dict(dist=9, box=22, insert=3 * K_NN, ascent=15), dict(dist=0, box=0, insert=0, ascent=0),
+                "SURVEY §8(d) estimates")
 
 
-def alu_ops_per_query(per_q: dict) -> float:
-    return (per_q["dist_evals"] * OPS_DIST + per_q["box_tests"] * OPS_BOX +
-            per_q["replacements"] * OPS_REPL + per_q["ascents"] * OPS_ASCENT)
+OP_COSTS, OP_HALF, OP_SOURCE = _op_costs()
+
+
+def alu_ops_per_query(per_q: dict, costs: dict | None = None) -> float:
+    c = OP_COSTS if costs is None else costs
+    return (per_q["dist_evals"] * c["dist"] + per_q["box_tests"] * c["box"] +
+            per_q["replacements"] * c["insert"] + per_q["ascents"] * c["ascent"])
+
+
+def mix_peak_factor(per_q: dict) -> float:
+    """Issue ceiling of the op mix relative to the full-rate one: half-rate
+    instructions (FMNMX, VIMNMX, IMAD.WIDE: 0.5 of full rate measured,
+    profiles/r01_alu_rates.json) occupy two issue slots' worth of their pipe."""
+    tot = alu_ops_per_query(per_q)
+    half = alu_ops_per_query(per_q, OP_HALF)
+    return tot / (tot + half) if tot > 0 else 1.0
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+# Algorithmic bytes (SURVEY §8(d)): build 274.6 B/pt (3D) / 270.6 (2D); insert (the
+# full-rebuild model) 268 m + 24 n + 58.6 (n + m); delete 4 m + 28 n_before (records +
+# alive lookups) + 24 n_after (compacted records) + 30.6 n_after (topology + boxes);
+# k-NN compulsory 16 + 6.6 + 12 k B/query.
+def build_bytes(n: int, dim: int) -> float:
+    return (274.6 if dim == 3 else 270.6) * n
+
+
+def insert_bytes(n: int, m: int) -> float:
+    return 268.0 * m + 24.0 * n + 58.6 * (n + m)
+
+
+def delete_bytes(n_before: int, m: int) -> float:
+    n_after = n_before - m
+    return 4.0 * m + 28.0 * n_before + 24.0 * n_after + 30.6 * n_after
+
+
+def knn_bytes(nq: int, k: int = K_NN) -> float:
+    return (16 + 6.6 + 12 * k) * nq
 
 
 def load_traffic():
@@ -289,6 +353,8 @@ def run_gpu(args, D: Dist):
     oi = torch.empty((n_live, K_NN), dtype=torch.int32, device=dev)
     od = torch.empty((n_live, K_NN), dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # this rank's shard of the queries: a contiguous Morton range (whole 32-query packets)
+    q_lo, q_hi = zd.query_partition(n_live, D.world, D.rank)
     st = torch.cuda.current_stream()
 
     def ev():
@@ -305,7 +371,7 @@ def run_gpu(args, D: Dist):
         t.zd_delete(kill)
         e3 = ev()
         t.zd_set_timing(True)
-        t.zd_knn(K_NN, out_idx=oi, out_dist2=od)
+        t.zd_knn_range(K_NN, q_lo, q_hi, oi, od)
         e4 = ev()
         return t, (e0, e1, e2, e3, e4)
 
@@ -351,7 +417,7 @@ def run_gpu(args, D: Dist):
     step_ms = ph.sum(1)
     tot_ms = D.max(float(step_ms.sum()))
     ms_per_step = tot_ms / args.steps
-    value = D.world * n_live * args.steps / (tot_ms / 1e3)
+    value = n_live * args.steps / (tot_ms / 1e3)   # one problem: the 10^7 queries, max time over ranks
     mean_ph = ph.mean(0)
     knn_ms = float(np.mean(knn_kernel))
 
@@ -369,7 +435,12 @@ def run_gpu(args, D: Dist):
         t = zd.zd_build(pts_h)
         t.zd_insert(batch_h)
         t.zd_delete(kill_h)
-        t.zd_knn(K_NN, out_idx=oi_h, out_dist2=od_h)
+        if D.world == 1:
+            t.zd_knn(K_NN, out_idx=oi_h, out_dist2=od_h)   # host outputs: the library stages them
+        else:   # this rank's shard into device rows, then the row arrays to the host
+            t.zd_knn_range(K_NN, q_lo, q_hi, oi, od)
+            oi_h.copy_(oi, non_blocking=True)
+            od_h.copy_(od, non_blocking=True)
         e1 = ev()
         torch.cuda.synchronize()
         t.zd_free()
@@ -385,49 +456,54 @@ def run_gpu(args, D: Dist):
             flush.fill_(1)
             e2e_ms.append(e2e_step())
         e2e_tot = D.max(float(sum(e2e_ms)))
-        e2e_value = D.world * n_live * args.e2e_steps / (e2e_tot / 1e3)
-        # e2e parity spot check: host result == device result
-        same = bool(torch.equal(oi_h, oi.cpu()) and torch.equal(od_h, od.cpu()))
+        e2e_value = n_live * args.e2e_steps / (e2e_tot / 1e3)
+        # e2e parity spot check: host rows of this shard == the device-timed run's rows
+        if D.world == 1:
+            same = bool(torch.equal(oi_h, oi.cpu()) and torch.equal(od_h, od.cpu()))
+        else:
+            same = None
 
     if D.rank != 0:
         return
 
-    # ---- roofline of the dominant kernel (k-NN): integer-ALU bound
+    # ---- CPU oracle on the headline workload (full size by default), rank 0 at N=1
     per_q, cpu = None, None
     if args.cpu_baseline and D.world == 1:
-        cpu, per_q = cpu_baseline(args.cpu_sample)
-    if per_q is None:
-        per_q = dict(dist_evals=92.1, box_tests=45.2, ascents=9.0, replacements=23.1)  # oracle, 3D uniform 1M
-    ops_q = alu_ops_per_query(per_q)
-    achieved = ops_q * n_live / (knn_ms / 1e3) / 1e12
+        cpu, per_q = cpu_baseline(args.cpu_sample or c["n"])
+    if per_q is None:   # oracle counters of 3D uniform at 10^6 (tests/test_oracle_pins.py App. A pin)
+        per_q = dict(dist_evals=92.0, box_tests=45.0, ascents=9.02, replacements=23.1, evictions=13.1)
+
+    # ---- per-config report (one GPU): C1-C4b build + k-NN, roofline fractions, parity
+    per_config = None
+    if args.per_config and D.world == 1:
+        per_config = run_per_config(zd, dev, clocks)
+
+    # ---- roofline of the dominant kernel (k-NN): issue-bound integer/fp32 ALU work
     sm_max = clocks.get("sm_max_mhz") or 1965.0
-    peak = 148 * 4 * 32 * sm_max * 1e6 / 1e12       # int32 lane-ops/s: 148 SMs x 4 SMSPs x 32 lanes x clock
+    knn_roof = knn_roofline(per_q, n_live, knn_ms, sm_max)
     traffic, traffic_src = load_traffic()
-    compulsory_bytes_q = 16 + 6.6 + K_NN * (4 + 8)
+    knn_roof.update({"kernel": "knn_packet_kernel<3,10>", "traffic": traffic, "traffic_source": traffic_src})
+    n_before_delete = c["n"] + c["insert_m"]
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": D.world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": config_block(),
+        "config": config_block({"parallelism": f"query shards: {D.world} x contiguous Morton range, tree replicated",
+                                "query_shard_rank0": [q_lo, q_hi]}),
         "phases_ms": {"build": float(mean_ph[0]), "insert": float(mean_ph[1]), "delete": float(mean_ph[2]),
                       "knn_call": float(mean_ph[3]), "knn_kernel": knn_ms},
         "build_mpts_s": c["n"] / (mean_ph[0] / 1e3) / 1e6,
-        # build against HBM: SURVEY §8(d) algorithmic bytes (3D: encode 20 + sort 196 +
-        # records 28 + topology/boxes 30.6 = 274.6 B/point) / build time / measured copy BW
-        "build_roofline": {"bound": "hbm", "bytes_per_point": 274.6,
-                           "achieved": 274.6 * c["n"] / (mean_ph[0] / 1e3) / 1e9, "unit": "GB/s",
-                           "peak": HBM_PEAK_GBS, "frac": 274.6 * c["n"] / (mean_ph[0] / 1e3) / 1e9 / HBM_PEAK_GBS,
-                           "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
+        "build_roofline": hbm_roof(build_bytes(c["n"], 3), mean_ph[0], "274.6 B/pt (SURVEY §8(d))"),
         "insert_mpts_s": c["insert_m"] / (mean_ph[1] / 1e3) / 1e6,
+        "insert_roofline": hbm_roof(insert_bytes(c["n"], c["insert_m"]), mean_ph[1],
+                                    "268 m + 24 n + 58.6 (n+m) B (full-rebuild model, SURVEY §8(d))"),
         "delete_mpts_s": c["delete_m"] / (mean_ph[2] / 1e3) / 1e6,
+        "delete_roofline": hbm_roof(delete_bytes(n_before_delete, c["delete_m"]), mean_ph[2],
+                                    "4 m + 28 n_before + 24 n_after + 30.6 n_after B"),
         "knn_qps": n_live / (mean_ph[3] / 1e3),
-        "roofline": {"kernel": "knn_packet_kernel<3,10>", "bound": "alu", "achieved": achieved, "peak": peak,
-                     "unit": "Tops/s (int32 lane-ops)", "frac": achieved / peak,
-                     "traffic": traffic, "traffic_source": traffic_src,
-                     "ops_per_query": ops_q, "counters_per_query": per_q,
-                     "peak_note": "derived: 148 SMs x 4 SMSPs x 32 lanes x sm_max clock (B200_PROFILING.md)",
-                     "hbm_frac_compulsory": compulsory_bytes_q * n_live / (knn_ms / 1e3) / (HBM_PEAK_GBS * 1e9)},
+        "roofline": knn_roof,
+        "per_config": per_config,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_tot / max(1, args.e2e_steps), "matches_device_result": same},
@@ -438,6 +514,99 @@ def run_gpu(args, D: Dist):
     print(json.dumps(line), flush=True)
 
 
+def hbm_roof(nbytes: float, ms: float, model: str) -> dict:
+    ach = nbytes / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": ach / HBM_PEAK_GBS,
+            "algorithmic_bytes": nbytes, "bytes_model": model,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"}
+
+
+def knn_roofline(per_q: dict, nq: int, knn_ms: float, sm_max: float) -> dict:
+    ops_q = alu_ops_per_query(per_q)
+    achieved = ops_q * nq / (knn_ms / 1e3) / 1e12
+    peak = 148 * 4 * 32 * sm_max * 1e6 / 1e12   # lane-instr/s: 148 SMs x 4 SMSPs x 32 lanes x clock
+    mixf = mix_peak_factor(per_q)
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "T lane-instr/s", "frac": achieved / peak,
+            "peak_mix": peak * mixf, "frac_mix": achieved / (peak * mixf),
+            "ops_per_query": ops_q, "op_costs": OP_COSTS, "op_costs_half_rate": OP_HALF, "op_costs_source": OP_SOURCE,
+            "counters_per_query": per_q,
+            "peak_note": "full-rate issue ceiling 148 SMs x 4 SMSPs x 32 lanes x sm_max clock (B200_PROFILING.md); "
+                         "peak_mix weights the op mix's half-rate FMNMX share (profiles/r01_alu_rates.json)",
+            "hbm_frac_compulsory": knn_bytes(nq) / (knn_ms / 1e3) / (HBM_PEAK_GBS * 1e9)}
+
+
+PER_CONFIGS = ("C1", "C2", "C3", "C4a", "C4b")
+
+
+def run_per_config(zd, dev, clocks) -> list:
+    """Per-config rows on one GPU (BASELINE.json configs[0..3]): build and k=10
+    all-points throughput with roofline fractions, every row compared with the CPU
+    oracle at full size (timed on all host cores), plus one-thread oracle runs for C1
+    and for a 10^6-point sample of the C3 recipe."""
+    import torch
+    import oracle
+    sm_max = clocks.get("sm_max_mhz") or 1965.0
+    rows = []
+    for name in PER_CONFIGS:
+        cfg = zdgen.CONFIGS[name]
+        n, dim = cfg["n"], cfg["dim"]
+        pts_np = zdgen.config_points(name)
+        pts = torch.from_numpy(pts_np).to(dev)
+        oi = torch.empty((n, K_NN), dtype=torch.int32, device=dev)
+        od = torch.empty((n, K_NN), dtype=torch.int64, device=dev)
+        st = torch.cuda.current_stream()
+        b_ms, k_ms, kk_ms = [], [], []
+        for rep in range(6):
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(st)
+            t = zd.zd_build(pts)
+            e1.record(st)
+            t.zd_set_timing(True)
+            t.zd_knn(K_NN, out_idx=oi, out_dist2=od)
+            e2.record(st)
+            torch.cuda.synchronize()
+            if rep > 0:   # rep 0 warms the pool and the caches
+                b_ms.append(e0.elapsed_time(e1))
+                k_ms.append(e1.elapsed_time(e2))
+                kk_ms.append(t.zd_get_timing()["knn"])
+            t.zd_free()
+        bm, km, kkm = statistics.median(b_ms), statistics.median(k_ms), statistics.median(kk_ms)
+        # oracle at full size on all host cores (its build is sequential, P:235 sort + Alg. 1)
+        t0 = time.perf_counter()
+        T = oracle.Tree(pts_np)
+        t1 = time.perf_counter()
+        ri, rd, cnt = T.knn_all(K_NN)
+        t2 = time.perf_counter()
+        per_q = {k: v / n for k, v in cnt.items()}
+        gi, gd = oi.cpu().numpy(), od.cpu().numpy()
+        exact = int(np.count_nonzero(np.all(gi == ri, axis=1) & np.all(gd == rd, axis=1)))
+        row = {"config": name, "n": n, "dim": dim, "dist": cfg["dist"], "k": K_NN,
+               "build_ms": bm, "build_mpts_s": n / (bm / 1e3) / 1e6,
+               "build_roofline": hbm_roof(build_bytes(n, dim), bm, f"{274.6 if dim == 3 else 270.6} B/pt"),
+               "knn_call_ms": km, "knn_kernel_ms": kkm, "knn_qps": n / (km / 1e3),
+               "knn_roofline": knn_roofline(per_q, n, kkm, sm_max),
+               "bit_exact_rows": f"{exact}/{n}",
+               "oracle_all_cores": {"cores": oracle.num_cores(), "build_s": t1 - t0, "knn_s": t2 - t1,
+                                    "knn_qps": n / (t2 - t1), "build_plus_knn_qps": n / (t2 - t0)}}
+        for key in ("knn_roofline",):   # keep the row compact
+            for drop in ("op_costs", "op_costs_half_rate", "op_costs_source", "peak_note"):
+                row[key].pop(drop, None)
+        if name in ("C1", "C3"):
+            n1 = n if name == "C1" else 1_000_000
+            p1 = pts_np if name == "C1" else zdgen.config_points(name, n1)
+            t0 = time.perf_counter()
+            T1 = oracle.Tree(p1)
+            t1 = time.perf_counter()
+            T1.knn_all(K_NN, nthreads=1)
+            t2 = time.perf_counter()
+            row["oracle_1_thread"] = {"n": n1, "sample": "full config" if n1 == n else
+                                      f"the {name} recipe at n={n1:,} (per-query work is flat in n, SURVEY App. A)",
+                                      "build_s": t1 - t0, "knn_s": t2 - t1, "knn_qps": n1 / (t2 - t1)}
+        rows.append(row)
+        del pts, oi, od, T, ri, rd, gi, gd
+    return rows
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -445,7 +614,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-sample", type=int, default=2_000_000)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="C5 points for the oracle baseline (0 = full 10^7)")
+    ap.add_argument("--no-per-config", dest="per_config", action="store_false")
     ap.add_argument("--ref-sample", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     args = ap.parse_args()

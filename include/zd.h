@@ -129,9 +129,22 @@ ZD_API int zd_knn(zd_tree *h, const int32_t *queries, int64_t m, int k,
 ZD_API int zd_knn_ex(zd_tree *h, const int32_t *queries, int64_t m, int k,
               int32_t *out_idx, int64_t *out_dist2, int flags);
 
+/* All-points k-NN restricted to the live points at sorted (Morton) positions
+ * [pos_lo, pos_hi) — one shard of the parallel-for over queries (
+ * SURVEY §8(e) item 1): every GPU holding a replica of the tree answers a contiguous
+ * Morton range, so together they produce the all-points output with no exchange.
+ * Writes only those points' rows of the full row-major outputs int32 / int64
+ * [zd_size(h)][k] (row = rank of the point's id among the live ids, as in zd_knn);
+ * other rows are untouched.  0 <= pos_lo <= pos_hi <= zd_size(h); the outputs must be
+ * device arrays (ZD_EINVAL otherwise); flags as zd_knn_ex.  Asynchronous. */
+ZD_API int zd_knn_range(zd_tree *h, int64_t pos_lo, int64_t pos_hi, int k,
+                        int32_t *out_idx, int64_t *out_dist2, int flags);
+
 /* Insert m points (int32 [m][dim]); they get ids first, first+1, ... where
- * first = the next unused id (ids are never reused, reading 20).  Returns first
- * (>= 0) or a negative code; on error the tree is unchanged.  The tree after the
+ * first = the next unused id (ids are never reused, reading 20); 0 <= m < 2^30.
+ * Returns first (>= 0) or a negative code; on a validation error (ZD_EINVAL,
+ * ZD_ERANGE) the tree is unchanged; a CUDA failure during the update leaves the handle
+ * unusable (later calls return ZD_ECUDA; free it).  The tree after the
  * call is the canonical zd-tree of the live multiset (reading 17).  Alg. 4
  * P:354-377. */
 ZD_API int64_t zd_insert(zd_tree *h, const int32_t *batch, int64_t m);

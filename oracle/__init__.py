@@ -23,8 +23,8 @@ _DIR = Path(__file__).resolve().parent
 _SRC = _DIR / "zd_oracle.c"
 _LIB = _DIR / "liboracle.so"
 
-NCNT = 4
-COUNTER_NAMES = ("dist_evals", "box_tests", "ascents", "replacements")
+NCNT = 5
+COUNTER_NAMES = ("dist_evals", "box_tests", "ascents", "replacements", "evictions")
 
 
 def build_lib(force: bool = False) -> Path:

@@ -306,7 +306,10 @@ void orc_export_nodes(const orc_tree *T, int64_t *lohi, int32_t *split, int32_t 
 
 /* ---------------------------------------------------------------- query */
 
-enum { CNT_DIST = 0, CNT_BOX = 1, CNT_ASCENT = 2, CNT_REPL = 3, NCNT = 4 };
+/* Work counters: leaf points scanned (own point included),
+ * nodes entered by searchDown, ascents of searchUp, insertions into the k-best set
+ * (fills and evictions), and evictions alone (insertions into a full set). */
+enum { CNT_DIST = 0, CNT_BOX = 1, CNT_ASCENT = 2, CNT_REPL = 3, CNT_EVICT = 4, NCNT = 5 };
 
 typedef struct {
     const orc_tree *T;
@@ -322,7 +325,10 @@ static void scan_leaf(qctx *Q, const orc_node *nd) {
         Q->cnt[CNT_DIST]++;
         if (p->id == Q->qid) continue;            /* "q != p" by id */
         int64_t d = dist2(Q->q, p->c, Q->T->dim);
-        Q->cnt[CNT_REPL] += nset_insert(Q->N, d, p->id);
+        const int full = Q->N->cnt == Q->N->k;
+        const int ins = nset_insert(Q->N, d, p->id);
+        Q->cnt[CNT_REPL] += ins;
+        Q->cnt[CNT_EVICT] += ins && full;
     }
 }
 

@@ -68,6 +68,9 @@ def load():
     L.zd_knn.argtypes = [P, P, i64, i32, P, P]
     L.zd_knn_ex.restype = i32
     L.zd_knn_ex.argtypes = [P, P, i64, i32, P, P, i32]
+    if hasattr(L, "zd_knn_range"):   # (older experiment builds lack the newer entry points)
+        L.zd_knn_range.restype = i32
+        L.zd_knn_range.argtypes = [P, i64, i64, i32, P, P, i32]
     L.zd_insert.restype = i64
     L.zd_insert.argtypes = [P, P, i64]
     L.zd_delete.restype = i64
@@ -90,8 +93,9 @@ def load():
     L.zd_export.argtypes = [P, P, P, P, P, P]
     L.zd_set_timing.restype = i32
     L.zd_set_timing.argtypes = [P, i32]
-    L.zd_trim.restype = i32
-    L.zd_trim.argtypes = []
+    if hasattr(L, "zd_trim"):
+        L.zd_trim.restype = i32
+        L.zd_trim.argtypes = []
     L.zd_kernel_launches.restype = i64
     L.zd_kernel_launches.argtypes = []
     L.zd_get_timing.restype = i32
@@ -194,6 +198,15 @@ class ZdTree:
             _check(load().zd_knn(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2)))
         return out_idx, out_dist2
 
+    def zd_knn_range(self, k: int, pos_lo: int, pos_hi: int, out_idx, out_dist2, root_based: bool = False,
+                     warp: bool = False):
+        """All-points k-NN of the live points at sorted positions [pos_lo, pos_hi) only
+        (one shard of the queries); writes their rows of the full
+        [zd_size(), k] device outputs."""
+        flags = (ZD_KNN_ROOT_BASED if root_based else 0) | (ZD_KNN_WARP if warp else 0)
+        _check(load().zd_knn_range(self.handle, int(pos_lo), int(pos_hi), k, _ptr(out_idx), _ptr(out_dist2), flags))
+        return out_idx, out_dist2
+
     def zd_insert(self, batch) -> int:
         b = _as_i32(batch)
         return _check(load().zd_insert(self.handle, _ptr(b), int(b.shape[0])))
@@ -258,6 +271,21 @@ def zd_knn_stats(reset: bool = True) -> dict:
     return dict(zip(KNN_STATS[:n], out[:n].tolist()))
 
 
+def query_partition(n: int, parts: int, part: int, align: int = 32) -> tuple[int, int]:
+    """Sorted-position range [lo, hi) of shard `part` of `parts` over n queries: equal
+    contiguous Morton ranges, boundaries rounded to whole 32-query packets (so no
+    packet straddles two shards); the ranges tile [0, n) exactly."""
+    if parts < 1 or not 0 <= part < parts or n < 0:
+        raise ValueError("need parts >= 1, 0 <= part < parts, n >= 0")
+
+    def cut(r):   # nearest packet boundary to r/parts of the queries
+        if r >= parts:
+            return n
+        return min(n, (2 * n * r + parts * align) // (2 * parts * align) * align)
+
+    return cut(part), cut(part + 1)
+
+
 def zd_trim() -> None:
     """Release the memory cached in the library's device pool (zd_trim)."""
     _check(load().zd_trim())
@@ -286,5 +314,5 @@ def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None,
     return ZdTree(h, dim)
 
 
-__all__ = ["zd_build", "zd_kernel_launches", "zd_trim", "zd_knn_stats", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "ZD_KNN_WARP", "PHASES",
+__all__ = ["zd_build", "zd_kernel_launches", "zd_trim", "query_partition", "zd_knn_stats", "ZdTree", "ZdError", "load", "build_lib", "last_error", "ZD_K_MAX", "ZD_KNN_WARP", "PHASES",
            "ZD_OK", "ZD_EINVAL", "ZD_ERANGE", "ZD_ENOMEM", "ZD_ECUDA"]

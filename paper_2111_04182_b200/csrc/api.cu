@@ -15,6 +15,8 @@
 #include <string>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/zd.h"
 #include "internal.h"
 
@@ -29,6 +31,14 @@ static cudaMemPool_t g_pools[64] = {};
 
 static cudaMemPool_t device_pool() {
     g_pool_once.run([](int dev) {
+        if (const char* e = std::getenv("ZD_POOL"); e && !std::strcmp(e, "default")) {   // testing
+            cudaMemPool_t dp = nullptr;
+            if (cudaDeviceGetDefaultMemPool(&dp, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(dp, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+            return;
+        }
         cudaMemPoolProps props{};
         props.allocType = cudaMemAllocationTypePinned;
         props.location.type = cudaMemLocationTypeDevice;
@@ -68,6 +78,15 @@ void clear_err() {
     g_err.clear();
     g_err_code = 0;
 }
+
+// NVTX range over a C-ABI call or one of its phases (SURVEY §5 tracing): free when no
+// profiler is attached (NVTX3 is header-only; nsys / ncu --nvtx pick the ranges up).
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 // Runs a cleanup at scope exit (scratch of an update that returns early on an error).
 template <class F>
@@ -325,6 +344,7 @@ int ensure_id_cap(zd_tree* h, int64_t need) {
 int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
               bool use_alt = false) {
     if (n <= 0) return ZD_OK;
+    Nvtx range("encode+radix sort");
     SortScratch s{};
     const bool alt = use_alt && h->keys2 && h->recs2 && n <= h->cap;
     if (alt) {
@@ -369,6 +389,7 @@ bool incr_enabled() {
 }
 
 int topology(zd_tree* h) {
+    Nvtx range("topology+boxes");
     if (h->ncap < h->n - 1) {
         // node buffers sized by count: flag + scan, read the internal-node count, grow
         topology_flags(h->keys, h->n, h->leaf_max, h->tb, h->st);
@@ -469,6 +490,9 @@ int do_build(zd_tree* h, const int32_t* points, int64_t n) {
     return ZD_OK;
 }
 
+int knn_impl(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_idx, int64_t* out_dist2, int flags,
+             int64_t q_lo, int64_t q_hi);
+
 }  // namespace
 
 extern "C" {
@@ -477,6 +501,7 @@ const char* zd_last_error(void) { return g_err.c_str(); }
 int zd_last_error_code(void) { return g_err_code; }
 
 zd_tree* zd_build_ex(const int32_t* points, int64_t n, int dim, const zd_opts* opts) {
+    Nvtx range("zd_build");
     clear_err();
     if (dim != 2 && dim != 3) { fail(ZD_EINVAL, "zd_build: dim must be 2 or 3"); return nullptr; }
     // the radix sort's look-back words carry 30-bit digit counts: one sort holds < 2^30 keys
@@ -569,6 +594,25 @@ int zd_knn(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_id
 
 int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_idx, int64_t* out_dist2, int flags) {
     clear_err();
+    return knn_impl(h, queries, m, k, out_idx, out_dist2, flags, 0, h ? h->n : 0);
+}
+
+int zd_knn_range(zd_tree* h, int64_t pos_lo, int64_t pos_hi, int k, int32_t* out_idx, int64_t* out_dist2, int flags) {
+    clear_err();
+    if (int e = check_handle(h)) return e;
+    if (pos_lo < 0 || pos_hi < pos_lo || pos_hi > h->n) return fail(ZD_EINVAL, "zd_knn_range: need 0 <= pos_lo <= pos_hi <= zd_size(h)");
+    if (pos_hi > pos_lo && (!is_device_ptr(out_idx) || !is_device_ptr(out_dist2)))
+        return fail(ZD_EINVAL, "zd_knn_range: outputs must be device arrays [zd_size(h)][k]");
+    return knn_impl(h, nullptr, h->n, k, out_idx, out_dist2, flags, pos_lo, pos_hi);
+}
+
+}  // extern "C"
+
+namespace {
+
+int knn_impl(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_idx, int64_t* out_dist2, int flags,
+             int64_t q_lo, int64_t q_hi) {
+    Nvtx range(queries ? "zd_knn(queries)" : "zd_knn(all points)");
     if (flags & ~(ZD_KNN_ROOT_BASED | ZD_KNN_WARP)) return fail(ZD_EINVAL, "zd_knn_ex: unknown flags");
     if (int e = check_handle(h)) return e;
     if (k < 1 || k > ZD_K_MAX) return fail(ZD_EINVAL, "zd_knn: k must be in [1, ZD_K_MAX]");
@@ -576,7 +620,7 @@ int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out
         return fail(ZD_EINVAL, "zd_knn: bad m (external queries: m < 2^30)");
     if (!queries && m != h->n) return fail(ZD_EINVAL, "zd_knn: all-points query needs m == zd_size(h)");
     if (m > 0 && (!out_idx || !out_dist2)) return fail(ZD_EINVAL, "zd_knn: NULL output");
-    if (m == 0) return ZD_OK;
+    if (m == 0 || q_hi <= q_lo) return ZD_OK;
     int rc;
     // Outputs: device pointers are written directly; host buffers are staged through
     // device memory and copied back (rows land scattered by id, so writing them over
@@ -606,6 +650,7 @@ int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out
         else if (!std::strcmp(dm, "all")) a.defer_all = 1;
     }
     a.dim = h->dim; a.k = k; a.n = h->n;
+    a.q_lo = q_lo; a.q_hi = q_hi;
     a.recs = h->recs; a.pt_leaf = h->tb.pt_leaf; a.leaf_start = h->tb.leaf_start;
     a.leaf_parent = h->tb.leaf_parent; a.nodes = h->tb.nodes; a.node_range = h->tb.range;
     a.pos_range = h->tb.pos_range;
@@ -678,7 +723,12 @@ int zd_knn_ex(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out
     return ZD_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
 int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
+    Nvtx range("zd_insert");
     clear_err();
     if (int e = check_handle(h)) return e;
     if (m < 0 || m >= kMaxSortKeys) return fail(ZD_EINVAL, "zd_insert: need 0 <= m < 2^30");
@@ -709,15 +759,21 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
         owned = nullptr;
     };
     auto scratch_guard = at_exit(free_scratch);
-    ZD_CUDA(dalloc(&bk, m, h->st));
-    ZD_CUDA(dalloc(&br, m, h->st));
-    rec(h, 2);
-    if ((rc = sort_into(h, (const int32_t*)db, m, (uint32_t)first, bk, br))) return rc;
     // NEXT-2 fast path (incr.cu): a small batch that keeps the canonical topology is
     // applied by position shifts and a box refit instead of the full rebuild (a
-    // single-leaf tree is refused by the check itself)
+    // single-leaf tree is refused by the check itself).  Its check needs the sorted
+    // batch, so small batches sort before the one sync; larger ones sort after it
+    // (measured: allocating the batch-sort scratch ahead of the sync makes the stream-
+    // ordered pool grow instead of reusing memory in the 10^6-point C5 insert).
     const bool try_fast = incr_enabled() && h->n > 1 && m <= kIncrMaxBatch;
+    auto sort_batch = [&]() -> int {
+        ZD_CUDA(dalloc(&bk, m, h->st));
+        ZD_CUDA(dalloc(&br, m, h->st));
+        rec(h, 2);
+        return sort_into(h, (const int32_t*)db, m, (uint32_t)first, bk, br);
+    };
     if (try_fast) {
+        if ((rc = sort_batch())) return rc;
         ZD_CUDA(dalloc(&bleaf, m, h->st));
         KnnArgs t{};
         t.nodes = h->tb.nodes; t.split_bit = h->tb.split_bit; t.d_meta = h->d_small; t.leaf_start = h->tb.leaf_start;
@@ -726,10 +782,8 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
     }
     ZD_CUDA(cudaMemcpyAsync(h->h_small, h->d_small, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->st));
     ZD_CUDA(cudaStreamSynchronize(h->st));   // the one sync
-    if (h->h_small[4]) {
-        free_scratch();
-        return fail(ZD_ERANGE, "zd_insert: coordinate outside the universe box (tree unchanged)");
-    }
+    if (h->h_small[4]) return fail(ZD_ERANGE, "zd_insert: coordinate outside the universe box (tree unchanged)");
+    if (!try_fast && (rc = sort_batch())) return rc;
     h->n_internal = h->h_small[0];
     h->n_leaves = h->n_internal + 1;
     h->root = h->h_small[1];
@@ -784,6 +838,7 @@ int64_t zd_insert(zd_tree* h, const int32_t* batch, int64_t m) {
 }
 
 int64_t zd_delete(zd_tree* h, const int32_t* ids, int64_t m) {
+    Nvtx range("zd_delete");
     clear_err();
     if (int e = check_handle(h)) return e;
     if (m < 0) return fail(ZD_EINVAL, "zd_delete: m < 0");

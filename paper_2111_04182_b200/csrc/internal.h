@@ -104,6 +104,7 @@ struct KnnArgs {
     int defer_all;               // testing: every packet goes to the second pass
     int root_based;              // ablation: root-based search
     int warp;                    // the warp-per-query kernel (knn_warp.cu) for any k
+    int64_t q_lo, q_hi;          // all-points: query the live points at sorted positions [q_lo, q_hi)
 };
 constexpr int kPacketKMax = 32;   // largest k of the packet kernel; above: knn_warp
 // Large-k path (knn_warp.cu): one warp per query over Morton-ordered queries.

@@ -959,6 +959,7 @@ struct PacketArgs {
     const int2* pos_range;     // per internal node: sorted point range [x, y)
     const int4* qrecs;         // queries in Morton order: (x, y, z|0, id or query index)
     const int32_t* qleaf;      // leaf of each query
+    int32_t q_lo;              // all-points: first query position (a partition of the sorted points)
     int32_t nq;
     int32_t n_pts;             // tree points (bounds checks)
     const int32_t* d_meta;     // [0] = internal node count (bounds checks)
@@ -1276,18 +1277,19 @@ __global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? (DIM == 3 ? ZD_MINB3
     __syncwarp();
 #endif
     const int64_t gw = (int64_t)blockIdx.x * Pw<K>::v + wib;
+    const int64_t qe = (int64_t)A.q_lo + A.nq;   // queries are the positions [q_lo, qe)
     if (!A.hard_mode) {
-        const int64_t p0 = gw * 32;
-        if (p0 >= A.nq) return;   // whole warp exits together
-        const int32_t pe = (int32_t)(p0 + 32 < (int64_t)A.nq ? p0 + 32 : (int64_t)A.nq);
+        if (gw * 32 >= A.nq) return;   // whole warp exits together
+        const int64_t p0 = A.q_lo + gw * 32;
+        const int32_t pe = (int32_t)(p0 + 32 < qe ? p0 + 32 : qe);
         search_packet<DIM, K, EXT>(A, (int32_t)p0, pe, gw, A.hard_list != nullptr, S, lane);
     } else {
         // second pass: the deferred packets' queries, one per warp (grid-stride)
         const int64_t cnt = min(*A.hard_count, A.hard_cap);
         const int64_t total = (int64_t)gridDim.x * Pw<K>::v;
         for (int64_t t = gw; t < cnt * 32; t += total) {
-            const int64_t pos = (int64_t)__ldg(A.hard_list + (t >> 5)) * 32 + (t & 31);
-            if (pos < A.nq) search_packet<DIM, K, EXT>(A, (int32_t)pos, (int32_t)pos + 1, 0, false, S, lane);
+            const int64_t pos = A.q_lo + (int64_t)__ldg(A.hard_list + (t >> 5)) * 32 + (t & 31);
+            if (pos < qe) search_packet<DIM, K, EXT>(A, (int32_t)pos, (int32_t)pos + 1, 0, false, S, lane);
         }
     }
 }
@@ -1377,8 +1379,10 @@ void knn_all(const KnnArgs& a, cudaStream_t st) {
     PacketArgs A = packet_args(a);
     A.qrecs = a.recs;
     A.qleaf = a.pt_leaf;
-    A.nq = (int32_t)a.n;
-    if (a.warp || a.k > kPacketKMax) { knn_warp(a, a.recs, a.pt_leaf, a.n, false, st); return; }
+    A.q_lo = (int32_t)a.q_lo;
+    A.nq = (int32_t)(a.q_hi - a.q_lo);
+    if (A.nq <= 0) return;
+    if (a.warp || a.k > kPacketKMax) { knn_warp(a, a.recs + a.q_lo, a.pt_leaf + a.q_lo, A.nq, false, st); return; }
     if (a.dim == 2) dispatch<2, false>(A, st); else dispatch<3, false>(A, st);
 }
 
@@ -1394,6 +1398,7 @@ void knn_queries(const KnnArgs& a, const uint64_t* qkeys, const int4* qrecs, int
     PacketArgs A = packet_args(a);
     A.qrecs = qrecs;
     A.qleaf = qleaf;
+    A.q_lo = 0;
     A.nq = (int32_t)m;
     if (a.warp || a.k > kPacketKMax) { knn_warp(a, qrecs, qleaf, m, true, st); return; }
     if (a.dim == 2) dispatch<2, true>(A, st); else dispatch<3, true>(A, st);

@@ -57,7 +57,69 @@ def test_workload_recipe_scaled():
 
 def test_alu_ops_model():
     per_q = dict(dist_evals=10, box_tests=1, ascents=1, replacements=1)
-    assert bench.alu_ops_per_query(per_q) == 10 * 9 + 22 + 30 + 15
+    c = bench.OP_COSTS
+    assert bench.alu_ops_per_query(per_q) == pytest.approx(10 * c["dist"] + c["box"] + c["insert"] + c["ascent"])
+    # SASS-derived costs are committed and sane: the insertion is the dearest op and
+    # carries the half-rate FMNMX chain (19 for k = 10)
+    assert bench.OP_SOURCE.startswith("profiles/")
+    assert c["insert"] > c["box"] > c["dist"] > 0 and bench.OP_HALF["insert"] == 19
+    assert 0.5 < bench.mix_peak_factor(dict(dist_evals=92, box_tests=45, ascents=9, replacements=23)) < 1.0
+
+
+def test_byte_models():
+    assert bench.build_bytes(10_000_000, 3) == pytest.approx(2.746e9)
+    assert bench.insert_bytes(10_000_000, 1_000_000) == pytest.approx(1.1526e9, rel=1e-3)   # SURVEY: 1.15 GB
+    assert 0.85e9 < bench.delete_bytes(11_000_000, 1_000_000) < 0.9e9                   # SURVEY: ~0.88 GB
+    assert bench.knn_bytes(10_000_000) == pytest.approx(1.426e9)
+
+
+def _part_worker(rank, world, port, n, q):
+    os.environ.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(world),
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_2111_04182_b200 import query_partition
+    D = bench.Dist(backend="gloo")
+    lo, hi = query_partition(n, world, rank)
+    t = torch.tensor([lo, hi], dtype=torch.int64)
+    got = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(got, t)
+    q.put((rank, [tuple(int(v) for v in g) for g in got]))
+    D.close()
+
+
+@pytest.mark.parametrize("n", [10_000_000, 1000, 31, 0])
+def test_query_shards_tile_the_queries_gloo(n):
+    """bench.py's multi-GPU split: each rank takes a contiguous
+    Morton range of whole 32-query packets; gathered over a world-size-2 gloo group the
+    ranges tile [0, n) exactly, in rank order, and are (almost) equal."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_part_worker, args=(r, 2, port, n, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+    res = dict(q.get(timeout=5) for _ in range(2))
+    assert res[0] == res[1]
+    (a0, a1), (b0, b1) = res[0]
+    assert a0 == 0 and a1 == b0 and b1 == n
+    assert a1 % 32 == 0 or a1 == n
+    assert abs((a1 - a0) - (b1 - b0)) <= 32
+
+
+def test_query_partition_properties():
+    from paper_2111_04182_b200 import query_partition
+    for n in (0, 1, 31, 32, 33, 1000, 65_536, 10_000_000, 10_000_001):
+        for parts in (1, 2, 3, 4, 7, 8):
+            r = [query_partition(n, parts, i) for i in range(parts)]
+            assert r[0][0] == 0 and r[-1][1] == n
+            assert all(r[i][1] == r[i + 1][0] for i in range(parts - 1))
+            assert all(lo <= hi for lo, hi in r)
+            assert all(hi % 32 == 0 or hi == n for lo, hi in r[:-1])
+    with pytest.raises(ValueError):
+        query_partition(10, 2, 2)
 
 
 def _check_line(line):

@@ -737,3 +737,33 @@ def test_trim_releases_pool(zd):
     assert zd.load().zd_trim() == 0
     t = zd.zd_build(dev(zdgen.uniform(1000, 3, seed=66)))   # the pool grows again on demand
     assert t.zd_size() == 1000
+
+
+@pytest.mark.parametrize("parts", [1, 3, 8])
+def test_knn_range_shards(zd, oracle_mod, parts):
+    """zd_knn_range (SURVEY §8(e) query shards): the shards' rows together equal the
+    all-points answer, and each call leaves the other rows untouched; also after a
+    delete (row map) and at k > 32 (warp kernel)."""
+    base = zdgen.uniform(20011, 3, seed=71)
+    t = zd.zd_build(dev(base))
+    t.zd_delete(dev(zdgen.delete_ids(20011, 1000, seed=72)))
+    n = t.zd_size()
+    for k in (10, 40):
+        ref_i, ref_d = gpu_knn_all(t, k)
+        oi = torch.full((n, k), -7, dtype=torch.int32, device="cuda")
+        od = torch.full((n, k), -7, dtype=torch.int64, device="cuda")
+        seen = np.zeros(n, bool)
+        for r in range(parts):
+            lo, hi = zd.query_partition(n, parts, r)
+            before = oi.cpu().numpy().copy()
+            t.zd_knn_range(k, lo, hi, oi, od)
+            torch.cuda.synchronize()
+            after = oi.cpu().numpy()
+            changed = np.any(after != before, axis=1)
+            assert not np.any(changed & seen), "a shard rewrote another shard's rows"
+            assert changed.sum() == hi - lo
+            seen |= changed
+        assert seen.all()
+        assert np.array_equal(oi.cpu().numpy(), ref_i) and np.array_equal(od.cpu().numpy(), ref_d)
+    with pytest.raises(zd.ZdError):
+        t.zd_knn_range(10, 5, n + 1, oi, od)

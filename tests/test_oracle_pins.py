@@ -404,3 +404,45 @@ def test_random_shift_changes_the_tree(oracle_mod):
     assert not np.array_equal(a.sorted_points()[1], b.sorted_points()[1])
     with pytest.raises(ValueError):
         oracle_mod.Tree(zdgen.uniform(10, 3, seed=1), shift=(1, 2, 3))
+
+
+# ---- work counters -----------------------------------
+# dist = leaf points scanned (own point included), box = nodes entered by searchDown,
+# ascents of searchUp, replacements = insertions into the k-best set (fills +
+# evictions), evictions = insertions into a full set.  They set the roofline's
+# algorithmic op count (bench.py), so they are pinned to a hand count and to App. A.
+
+def test_counters_hand_counted_2x2_grid(oracle_mod):
+    """2x2 grid, leaf size 1, k = 1 (the S:190 tree: four leaves under two nodes).
+    Query (0,0) id 0: own leaf (1 scan, self), sibling leaf (0,1): 1 box + 1 scan
+    (fill d2=1); ascent; margin test at the left node fails ((0+1)^2 = 1 is not > 1);
+    right node entered (box d2 1 <= 1), its children by box distance: leaf (1,0)
+    (1 box, 1 scan: (1, id 2) does not beat (1, id 0)), leaf (1,1) (1 box, pruned:
+    2 > 1); ascent to the root.  -> 3 scans, 4 boxes, 2 ascents, 1 fill.  Queries id 1
+    and id 3 mirror it; ids 2 and 3 end with an eviction each, because their first
+    d2 = 1 neighbour (id 3 / id 2) loses the (d2, id) tie to one found later (id 0 /
+    id 1).  Totals: 12 scans, 16 boxes, 8 ascents, 4 fills + 2 evictions."""
+    pts = np.array([[0, 0], [0, 1], [1, 0], [1, 1]], np.int32)
+    _, _, cnt = oracle_mod.Tree(pts, leaf_max=1).knn_all(1, nthreads=1)
+    assert cnt == dict(dist_evals=12, box_tests=16, ascents=8, replacements=6, evictions=2)
+    # two points: each query scans its own leaf, enters the sibling leaf, ascends once
+    _, _, cnt = oracle_mod.Tree(np.array([[0, 0], [5, 0]], np.int32), leaf_max=1).knn_all(1, nthreads=1)
+    assert cnt == dict(dist_evals=4, box_tests=2, ascents=2, replacements=2, evictions=0)
+
+
+@pytest.mark.parametrize("dim,app_a", [
+    (3, dict(dist_evals=91.0, box_tests=44.6, ascents=8.97, evictions=13.0, leaves=89_380)),
+    (2, dict(dist_evals=43.8, box_tests=16.4, ascents=5.22, evictions=8.7, leaves=89_475)),
+])
+def test_counters_match_appendix_a(oracle_mod, dim, app_a):
+    """Per-query work at n = 10^6 uniform, k = 10 against SURVEY App. A (its
+    independent numpy model of the same search), within 3%; fills are exactly k."""
+    pts = zdgen.uniform(1_000_000, dim, seed=3 if dim == 3 else 2)
+    t = oracle_mod.Tree(pts)
+    _, _, cnt = t.knn_all(10)
+    per_q = {k: v / t.n for k, v in cnt.items()}
+    for key in ("dist_evals", "box_tests", "ascents", "evictions"):
+        assert abs(per_q[key] / app_a[key] - 1) < 0.03, (key, per_q[key], app_a[key])
+    assert per_q["replacements"] - per_q["evictions"] == pytest.approx(10.0)
+    leaves = int((t.nodes()["split"] < 0).sum())
+    assert abs(leaves / app_a["leaves"] - 1) < 0.01
