@@ -620,7 +620,7 @@ int knn_impl(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_
         return fail(ZD_EINVAL, "zd_knn: bad m (external queries: m < 2^30)");
     if (!queries && m != h->n) return fail(ZD_EINVAL, "zd_knn: all-points query needs m == zd_size(h)");
     if (m > 0 && (!out_idx || !out_dist2)) return fail(ZD_EINVAL, "zd_knn: NULL output");
-    if (m == 0 || q_hi <= q_lo) return ZD_OK;
+    if (m == 0 || (!queries && q_hi <= q_lo)) return ZD_OK;   // (an empty shard writes nothing)
     int rc;
     // Outputs: device pointers are written directly; host buffers are staged through
     // device memory and copied back (rows land scattered by id, so writing them over
