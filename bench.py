@@ -536,6 +536,7 @@ def knn_roofline(per_q: dict, nq: int, knn_ms: float, sm_max: float) -> dict:
 
 
 PER_CONFIGS = ("C1", "C2", "C3", "C4a", "C4b")
+C3_SHIFT = (1234567, 765432, 1048577)   # a fixed 3D shift in [0, 2^21)^3 for the C3+shift row
 
 
 def run_per_config(zd, dev, clocks) -> list:
@@ -603,6 +604,29 @@ def run_per_config(zd, dev, clocks) -> list:
                                       f"the {name} recipe at n={n1:,} (per-query work is flat in n, SURVEY App. A)",
                                       "build_s": t1 - t0, "knn_s": t2 - t1, "knn_qps": n1 / (t2 - t1)}
         rows.append(row)
+        if name == "C3":   # NEXT-4: the same config with the 3D random shift (reading R31)
+            sh = C3_SHIFT
+            b_ms, k_ms = [], []
+            for rep in range(4):
+                e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                e0.record(st)
+                t = zd.zd_build(pts, shift=sh)
+                e1.record(st)
+                t.zd_set_timing(True)
+                t.zd_knn(K_NN, out_idx=oi, out_dist2=od)
+                e2.record(st)
+                torch.cuda.synchronize()
+                if rep > 0:
+                    b_ms.append(e0.elapsed_time(e1))
+                    k_ms.append(t.zd_get_timing()["knn"])
+                t.zd_free()
+            gi, gd = oi.cpu().numpy(), od.cpu().numpy()
+            exact = int(np.count_nonzero(np.all(gi == ri, axis=1) & np.all(gd == rd, axis=1)))
+            bm, kkm = statistics.median(b_ms), statistics.median(k_ms)
+            rows.append({"config": "C3+shift", "shift": list(sh), "n": n, "dim": dim, "k": K_NN,
+                         "build_ms": bm, "build_mpts_s": n / (bm / 1e3) / 1e6, "knn_kernel_ms": kkm,
+                         "knn_qps_kernel": n / (kkm / 1e3),
+                         "bit_exact_rows_vs_unshifted_oracle": f"{exact}/{n}"})
         del pts, oi, od, T, ri, rd, gi, gd
     return rows
 

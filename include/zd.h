@@ -86,13 +86,16 @@ typedef struct zd_opts {
                        keys equal); 0 = default 16; valid 1..ZD_LEAF_MAX_MAX */
     int timing;     /* nonzero: record per-phase device times (zd_get_timing) */
     /* Random shift (§2, "select a random shift ... kept throughout"; Lemma 2.2
-     * P:450): shift_set != 0 adds shift[a] in [0, 2^30) to axis a of every point —
-     * build points, inserted batches and external queries alike — after the range
-     * check and before encoding.  2D only: shifted coordinates need 31 bits per axis
-     * (62-bit keys); in 3D they would need 22 bits (66-bit keys), so dim 3 with
-     * shift_set returns ZD_EINVAL.  Distances, neighbour ids and rows are unchanged
-     * (a translation); the tree is the canonical tree of the shifted points and
-     * zd_export reports shifted keys and coordinates.  The caller draws the shift. */
+     * P:450): shift_set != 0 adds shift[a] to axis a of every point — build points,
+     * inserted batches and external queries alike — after the range check and before
+     * encoding.  2D: shift[a] in [0, 2^30), shifted coordinates of 31 bits, 62-bit
+     * keys.  3D: shift[a] in [0, 2^21), shifted coordinates of 22 bits; the key
+     * interleaves their levels 21..1 (63 bits: the Morton order of the shifted grid at
+     * cell size 2, DESIGN reading R31) while records keep the exact shifted
+     * coordinates.  Other shifts return ZD_EINVAL.  Distances, neighbour ids and rows
+     * are unchanged (a translation); the tree is the canonical tree of the shifted
+     * points and zd_export reports shifted keys and coordinates.  The caller draws the
+     * shift. */
     int shift_set;
     int32_t shift[3];
 } zd_opts;

@@ -58,6 +58,8 @@ def lib():
         L.orc_build.argtypes = [P, P, i64, i32, i32]
         L.orc_build_bits.restype = P
         L.orc_build_bits.argtypes = [P, P, i64, i32, i32, i32]
+        L.orc_build_levels.restype = P
+        L.orc_build_levels.argtypes = [P, P, i64, i32, i32, i32, i32]
         L.orc_free.argtypes = [P]
         L.orc_size.restype = i64
         L.orc_size.argtypes = [P]
@@ -130,21 +132,23 @@ class Tree:
     """Oracle zd-tree over (points, ids).
 
     shift: the random shift of P:235 ("select a random shift ... kept throughout"),
-    2D only: (sx, sy) in [0, 2^30) is added to every point (and query) and the keys
-    take 31 bits per axis.  The tree then stores the shifted coordinates."""
+    added to every point (and query); the tree then stores the shifted coordinates.
+    2D: (sx, sy) in [0, 2^30), keys of 31 bits per axis (62 bits).  3D: (sx, sy, sz)
+    in [0, 2^21), shifted coordinates of 22 bits; the key interleaves their levels
+    21 .. 1 (63 bits: the Morton order of the shifted grid at cell size 2; DESIGN
+    reading R31)."""
 
     def __init__(self, points: np.ndarray, ids: np.ndarray | None = None, leaf_max: int = 16, shift=None):
         pts = _c32(points)
         self.shift = None if shift is None else np.asarray(shift, np.int64)[: pts.shape[1]]
         if self.shift is not None:
-            if pts.shape[1] != 2:
-                raise ValueError("the random shift is 2D only (3D would need 66-bit keys)")
             pts = _c32((pts.astype(np.int64) + self.shift).astype(np.int32))
         self.points = pts
         self.n, self.dim = self.points.shape
         self.ids = np.arange(self.n, dtype=np.int32) if ids is None else _c32(ids)
         bits = (30 if self.dim == 2 else 21) + (1 if self.shift is not None else 0)
-        self._h = lib().orc_build_bits(_p(self.points), _p(self.ids), self.n, self.dim, leaf_max, bits)
+        lo = 1 if (self.shift is not None and self.dim == 3) else 0
+        self._h = lib().orc_build_levels(_p(self.points), _p(self.ids), self.n, self.dim, leaf_max, bits, lo)
         if not self._h:
             raise ValueError("orc_build failed")
         self.leaf_max = leaf_max

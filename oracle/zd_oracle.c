@@ -45,13 +45,15 @@ static int bits_per_axis(int dim) { return dim == 2 ? 30 : 21; }
 /* "taking each integer coordinate in binary form, interleaving the
  * coordinates to create one integer per point".  Level l = B-1 .. 0, axis
  * 0 .. dim-1, key = (key << 1) | bit. */
-static uint64_t key_bits(const int32_t *c, int dim, int B) {
+static uint64_t key_levels(const int32_t *c, int dim, int B, int lo) {
     uint64_t key = 0;
-    for (int l = B - 1; l >= 0; --l)
+    for (int l = B - 1; l >= lo; --l)
         for (int a = 0; a < dim; ++a)
             key = (key << 1) | (uint64_t)(((uint32_t)c[a] >> l) & 1u);
     return key;
 }
+
+static uint64_t key_bits(const int32_t *c, int dim, int B) { return key_levels(c, dim, B, 0); }
 
 uint64_t orc_key(const int32_t *c, int dim) { return key_bits(c, dim, bits_per_axis(dim)); }
 
@@ -168,7 +170,8 @@ typedef struct orc_tree {
     int32_t nnodes, cap, root;
     int32_t *leaf_of;   /* sorted position -> leaf node */
     int64_t *row_of;    /* sorted position -> output row (rank of id among ids) */
-    int bits;          /* key bits per axis */
+    int bits;          /* key bits per axis: levels bits-1 .. lo of every coordinate */
+    int lo;            /* lowest level in the key (1 in the 3D random-shift mode, else 0) */
 } orc_tree;
 
 static int cmp_pt(const void *a, const void *b) {
@@ -243,10 +246,16 @@ static int cmp_i32(const void *a, const void *b) {
  * keys of `bits` bits per axis.  The random shift (§2, "select a random shift
  * ... kept throughout") is applied by the caller to the coordinates it passes, which
  * then need one more bit per axis (2D: 31). */
-orc_tree *orc_build_bits(const int32_t *pts, const int32_t *ids, int64_t n, int dim, int leaf_max, int bits) {
-    if ((dim != 2 && dim != 3) || n < 0 || leaf_max < 1 || bits < 1 || bits * dim > 64) return NULL;
+/* Keys of the levels bits-1 .. lo of every coordinate ((bits - lo) * dim key bits).
+ * The 3D random shift (DESIGN reading R31) makes coordinates 22-bit; its key takes the
+ * levels 21 .. 1 (63 bits: the Morton order of the shifted grid at cell size 2), with
+ * the exact coordinates kept for every distance. */
+orc_tree *orc_build_levels(const int32_t *pts, const int32_t *ids, int64_t n, int dim, int leaf_max, int bits,
+                           int lo) {
+    if ((dim != 2 && dim != 3) || n < 0 || leaf_max < 1 || bits < 1 || lo < 0 || lo >= bits ||
+        (bits - lo) * dim > 64) return NULL;
     orc_tree *T = (orc_tree *)calloc(1, sizeof(orc_tree));
-    T->dim = dim; T->leaf_max = leaf_max; T->n = n; T->bits = bits;
+    T->dim = dim; T->leaf_max = leaf_max; T->n = n; T->bits = bits; T->lo = lo;
     T->pts = (orc_pt *)malloc(sizeof(orc_pt) * (size_t)(n ? n : 1));
     T->leaf_of = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
     T->row_of = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n ? n : 1));
@@ -254,7 +263,7 @@ orc_tree *orc_build_bits(const int32_t *pts, const int32_t *ids, int64_t n, int 
         orc_pt *p = &T->pts[i];
         p->id = ids ? ids[i] : (int32_t)i;
         p->c[0] = pts[i * dim]; p->c[1] = pts[i * dim + 1]; p->c[2] = dim == 3 ? pts[i * dim + 2] : 0;
-        p->key = key_bits(&pts[i * dim], dim, bits);
+        p->key = key_levels(&pts[i * dim], dim, bits, lo);
     }
     qsort(T->pts, (size_t)n, sizeof(orc_pt), cmp_pt);
     T->root = build_rec(T, 0, n, -1);
@@ -268,6 +277,10 @@ orc_tree *orc_build_bits(const int32_t *pts, const int32_t *ids, int64_t n, int 
     }
     free(sid);
     return T;
+}
+
+orc_tree *orc_build_bits(const int32_t *pts, const int32_t *ids, int64_t n, int dim, int leaf_max, int bits) {
+    return orc_build_levels(pts, ids, n, dim, leaf_max, bits, 0);
 }
 
 orc_tree *orc_build(const int32_t *pts, const int32_t *ids, int64_t n, int dim, int leaf_max) {
@@ -424,7 +437,7 @@ static void *run_job(void *arg) {
             Q.q = qc; Q.qid = INT32_MIN;        /* dynamic query: nothing excluded */
             row = t;
             if (T->n == 0) { /* empty tree: nothing to search */ }
-            else if (J->mode == MODE_EXT_BIT) search_up(&Q, locate_leaf(T, key_bits(qc, T->dim, T->bits)));
+            else if (J->mode == MODE_EXT_BIT) search_up(&Q, locate_leaf(T, key_levels(qc, T->dim, T->bits, T->lo)));
             else search_down(&Q, T->root);
         }
         write_row(&N, k, J->oi + row * k, J->od + row * k);

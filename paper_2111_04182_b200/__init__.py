@@ -298,8 +298,9 @@ def zd_kernel_launches() -> int:
 
 def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None, timing: bool = False,
              shift=None) -> ZdTree:
-    """Build a zd-tree over int32 points [n, dim] (point i gets id i).  shift: 2D
-    random shift (sx, sy) in [0, 2^30) applied to every point (zd_opts.shift)."""
+    """Build a zd-tree over int32 points [n, dim] (point i gets id i).  shift: the
+    random shift of P:235 applied to every point (zd_opts.shift): 2D (sx, sy) in
+    [0, 2^30); 3D (sx, sy, sz) in [0, 2^21)."""
     p = _as_i32(points)
     n = int(p.shape[0])
     dim = int(p.shape[1]) if dim is None else dim

@@ -184,7 +184,7 @@ struct zd_tree {
     int64_t fast_inserts = 0;   // inserts applied by the NEXT-2 fast path (introspection/tests)
     int64_t fast_deletes = 0;   // deletes applied by the NEXT-2 fast path
     bool shift_set = false;
-    int32_t shift[3] = {0, 0, 0};   // 2D random shift, applied before encoding
+    int32_t shift[3] = {0, 0, 0};   // random shift, applied before encoding
     // sorted live points
     uint64_t* keys = nullptr;
     int4* recs = nullptr;
@@ -517,9 +517,12 @@ zd_tree* zd_build_ex(const int32_t* points, int64_t n, int dim, const zd_opts* o
     if (leaf_max < 1 || leaf_max > ZD_LEAF_MAX_MAX) { fail(ZD_EINVAL, "zd_build: leaf_max out of range"); return nullptr; }
     const bool shift_set = opts && opts->shift_set;
     if (shift_set) {
-        if (dim != 2) { fail(ZD_EINVAL, "zd_build: the random shift needs 66-bit keys in 3D (2D only)"); return nullptr; }
-        for (int a = 0; a < 2; ++a)
-            if (opts->shift[a] < 0 || opts->shift[a] >= (1 << 30)) { fail(ZD_EINVAL, "zd_build: shift outside [0, 2^30)"); return nullptr; }
+        const int lim = dim == 2 ? (1 << 30) : (1 << 21);   // shifted axes: 31 / 22 bits
+        for (int a = 0; a < dim; ++a)
+            if (opts->shift[a] < 0 || opts->shift[a] >= lim) {
+                fail(ZD_EINVAL, dim == 2 ? "zd_build: shift outside [0, 2^30)" : "zd_build: shift outside [0, 2^21)");
+                return nullptr;
+            }
     }
     zd_tree* h = new zd_tree();
     h->dim = dim;
@@ -528,8 +531,7 @@ zd_tree* zd_build_ex(const int32_t* points, int64_t n, int dim, const zd_opts* o
     h->timing = timing;
     if (shift_set) {
         h->shift_set = true;
-        h->shift[0] = opts->shift[0];
-        h->shift[1] = opts->shift[1];
+        for (int a = 0; a < dim; ++a) h->shift[a] = opts->shift[a];
     }
     if (do_build(h, points, n) != ZD_OK) {
         std::string e = g_err;

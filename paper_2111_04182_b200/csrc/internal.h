@@ -50,7 +50,9 @@ size_t sort_zero_words(int64_t n);
 // Encode pts (int32 [n][dim]) and sort; ids = id_base + i.  Writes sorted keys
 // and records int4(x, y, z|0, id).  Sets *d_invalid != 0 if a coordinate is out of
 // the universe box.
-// shift2: the 2D random shift (int32 [2]) added after the range check, or NULL.
+// shift2: the random shift (int32 [dim]) added after the range check, or NULL (2D:
+// 62-bit keys; 3D: keys of the shifted coordinates' levels 21..1, records gathered
+// from the input points).
 void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out,
                  int4* recs_out, const SortScratch& s, int* d_invalid, cudaStream_t st,
                  const int32_t* shift2 = nullptr);

@@ -11,6 +11,9 @@
 // digit order and scatters runs of equal digits coalesced.  Pass 1 reads the
 // int32 points directly (encode fused, ids = iota); the last pass decodes the
 // coordinates from the key and writes the 16-byte records (K3 fused).
+#include <cstdio>
+#include <cstdlib>
+
 #include <cuda/atomic>
 
 #include "common.cuh"
@@ -43,21 +46,30 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
     cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(*p).store(v, cuda::memory_order_relaxed);
 }
 
-// Range check in the universe box, then the 2D random shift (zero when unset).
+// Random shift applied after the range check: sh = (sx, sy, sz, mode), mode 0
+// none, 2: 2D (31-bit shifted axes, 62-bit keys), 3: 3D (22-bit shifted axes; the key
+// interleaves their levels 21..1 = 63 bits, reading R31).
+template <int DIM>
+__device__ __forceinline__ uint64_t shifted_key(int x, int y, int z, int4 sh) {
+    if (DIM == 2) return morton<2>(x + sh.x, y + sh.y, 0);
+    if (sh.w == 3) return morton<3>((x + sh.x) >> 1, (y + sh.y) >> 1, (z + sh.z) >> 1);
+    return morton<3>(x, y, z);
+}
+
+// Range check in the universe box, then the key of the (shifted) point.
 template <int DIM>
 __device__ __forceinline__ uint64_t load_key_from_points(const int32_t* __restrict__ pts, uint32_t i, bool& bad,
-                                                         int2 sh) {
+                                                         int4 sh) {
     const int32_t* p = pts + (size_t)i * DIM;
     int x = __ldg(p), y = __ldg(p + 1), z = DIM == 3 ? __ldg(p + 2) : 0;
     bad |= !in_universe<DIM>(x, y, z);
-    if (DIM == 2) { x += sh.x; y += sh.y; }
-    return morton<DIM>(x, y, z);
+    return shifted_key<DIM>(x, y, z, sh);
 }
 
 // Up-front histogram of all 8 digits (+ range validation).
 template <int DIM>
 __global__ void __launch_bounds__(256) hist_kernel(const int32_t* __restrict__ pts, uint32_t n,
-                                                   uint32_t* __restrict__ g_hist, int* __restrict__ invalid, int2 sh2,
+                                                   uint32_t* __restrict__ g_hist, int* __restrict__ invalid, int4 sh2,
                                                    uint64_t* __restrict__ keys_out) {
     __shared__ uint32_t sh[NPASS][256];
     for (int i = threadIdx.x; i < NPASS * 256; i += 256) (&sh[0][0])[i] = 0;
@@ -90,7 +102,7 @@ __global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
     const int32_t* __restrict__ pts, const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ ids_in,
     uint64_t* __restrict__ keys_out, uint32_t* __restrict__ ids_out, int4* __restrict__ recs_out,
     uint32_t n, int shift, uint32_t id_base, const uint32_t* __restrict__ digit_offs,
-    uint32_t* status, uint32_t* tile_counter, int2 psh) {
+    uint32_t* status, uint32_t* tile_counter, int4 psh) {
     __shared__ union {
         uint32_t hist[SW][256];
         uint64_t keys[STILE];
@@ -231,7 +243,17 @@ __global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
         uint32_t dest = s_glob[d] + i;
         ZD_DCHECK(dest < n);
         keys_out[dest] = k;
-        if (MODE == 2) recs_out[dest] = decode_rec<DIM>(k, (int)s_ids[i]);
+        if (MODE == 2) {
+            if (DIM == 3 && psh.w == 3) {
+                // 3D shift: the key drops each coordinate's lowest bit, so the record
+                // comes from the input point (ids of a sort are id_base + input index)
+                const uint32_t id = s_ids[i];
+                const int32_t* p = pts + (size_t)(id - id_base) * 3;
+                recs_out[dest] = make_int4(__ldg(p) + psh.x, __ldg(p + 1) + psh.y, __ldg(p + 2) + psh.z, (int)id);
+            } else {
+                recs_out[dest] = decode_rec<DIM>(k, (int)s_ids[i]);
+            }
+        }
         else ids_out[dest] = s_ids[i];
     }
     (void)bad;
@@ -239,19 +261,31 @@ __global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
 
 template <int DIM>
 void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
-                   const SortScratch& s, int* d_invalid, int2 psh, cudaStream_t st) {
+                   const SortScratch& s, int* d_invalid, int4 psh, cudaStream_t st) {
     const uint32_t un = (uint32_t)n;
     const size_t tiles = sort_tiles(n);
     uint32_t* hist = s.zero_block;
     uint32_t* counters = hist + NPASS * 256;
     uint32_t* status = counters + NPASS;
+    // development aid: ZD_SORT_PROFILE=1 prints per-kernel device times of each sort
+    static const bool prof = std::getenv("ZD_SORT_PROFILE") != nullptr;
+    cudaEvent_t pev[NPASS + 4] = {};
+    int npev = 0;
+    auto mark = [&]() {
+        if (!prof) return;
+        cudaEventCreate(&pev[npev]);
+        cudaEventRecord(pev[npev++], st);
+    };
+    mark();
     cudaMemsetAsync(s.zero_block, 0, sort_zero_words(n) * sizeof(uint32_t), st);
+    mark();
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int hb = (int)std::min<size_t>((size_t)sms * 8, (n + 255) / 256);
     hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid, psh, s.k[1]);
     scan_hist_kernel<<<1, 256, 0, st>>>(hist, s.offs);
+    mark();
     count_launch(2 + NPASS);
     for (int p = 0; p < NPASS; ++p) {
         uint32_t* stp = status + (size_t)p * tiles * 256;
@@ -263,8 +297,21 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
             onesweep_kernel<DIM, 1><<<tiles, ST, 0, st>>>(nullptr, s.k[(p - 1) & 1], s.v[(p - 1) & 1], s.k[p & 1],
                                                           s.v[p & 1], nullptr, un, 8 * p, 0, off, stp, counters + p, psh);
         else
-            onesweep_kernel<DIM, 2><<<tiles, ST, 0, st>>>(nullptr, s.k[(p - 1) & 1], s.v[(p - 1) & 1], keys_out,
-                                                          nullptr, recs_out, un, 8 * p, 0, off, stp, counters + p, psh);
+            onesweep_kernel<DIM, 2><<<tiles, ST, 0, st>>>(pts, s.k[(p - 1) & 1], s.v[(p - 1) & 1], keys_out,
+                                                          nullptr, recs_out, un, 8 * p, id_base, off, stp, counters + p,
+                                                          psh);
+        mark();
+    }
+    if (prof) {
+        cudaEventSynchronize(pev[npev - 1]);
+        fprintf(stderr, "sort n=%lld:", (long long)n);
+        for (int i = 1; i < npev; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, pev[i - 1], pev[i]);
+            fprintf(stderr, " %.1f", ms * 1e3f);
+        }
+        fprintf(stderr, " us\n");
+        for (int i = 0; i < npev; ++i) cudaEventDestroy(pev[i]);
     }
 }
 
@@ -276,9 +323,10 @@ size_t sort_zero_words(int64_t n) { return NPASS * 256 + NPASS + (size_t)NPASS *
 void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
                  const SortScratch& s, int* d_invalid, cudaStream_t st, const int32_t* shift2) {
     if (n <= 0) return;
-    const int2 psh = shift2 ? make_int2(shift2[0], shift2[1]) : make_int2(0, 0);
+    const int4 psh = shift2 ? make_int4(shift2[0], shift2[1], dim == 3 ? shift2[2] : 0, dim)
+                            : make_int4(0, 0, 0, 0);
     if (dim == 2) sort_points_t<2>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st);
-    else sort_points_t<3>(pts, n, id_base, keys_out, recs_out, s, d_invalid, make_int2(0, 0), st);
+    else sort_points_t<3>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st);
 }
 
 }  // namespace zd

@@ -113,3 +113,19 @@ def test_config_full_fast_updates(zd, oracle_mod, monkeypatch):
     ex2 = t.zd_export()
     for key in ("keys", "recs", "leaf_start", "leaf_parent", "nodes"):
         assert np.array_equal(ex2[key], ex[key]), key
+
+
+def test_config_full_shift_3d(zd, oracle_mod):
+    """C3 with the 3D random shift (reading R31) at full size: the tree equals
+    the shifted oracle's canonical tree (node count) and every row equals the
+    oracle's unshifted answer (a translation)."""
+    pts = zdgen.config_points("C3")
+    sh = (1234567, 765432, 1048577)
+    t = zd.zd_build(torch.from_numpy(pts).cuda(), shift=sh)
+    gi, gd = t.zd_knn(K)
+    torch.cuda.synchronize()
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(K)
+    bad = first_row_mismatch(gi.cpu().numpy(), gd.cpu().numpy(), oi, od)
+    assert bad.size == 0, f"{bad.size} rows differ"
+    st = oracle_mod.Tree(pts, shift=sh)
+    assert t.zd_get_info()["n_internal"] == (st.nodes()["split"] >= 0).sum()

@@ -498,10 +498,48 @@ def test_random_shift(zd, oracle_mod, dist, leaf_max, shift):
     check_rows(*gpu_knn_all(t, 10), oi, od)
 
 
+SHIFTS3 = [(0, 0, 0), (1, 2, 3), ((1 << 21) - 1, (1 << 21) - 1, (1 << 21) - 1), (1234567, 7654, 1 << 20)]
+
+
+@pytest.mark.parametrize("shift", SHIFTS3)
+@pytest.mark.parametrize("dist,leaf_max", [("uniform", 16), ("plummer", 16), ("sphere", 16), ("dup", 16),
+                                           ("uniform", 1)])
+def test_random_shift_3d(zd, oracle_mod, dist, leaf_max, shift):
+    """3D random shift (reading R31): the canonical tree over the keys of the
+    shifted coordinates' levels 21..1 equals the oracle's, and every answer equals the
+    unshifted tree's (a translation), for all-points, external queries and updates
+    (fast and full paths)."""
+    pts = zdgen.points(dist, 12000, 3, seed=85)
+    t = zd.zd_build(dev(pts), leaf_max=leaf_max, shift=shift)
+    assert t.zd_get_info()["shift"] == list(shift)
+    live = oracle_mod.LiveSet(pts, leaf_max=leaf_max, shift=shift)
+    assert_same_structure(t.zd_export(), live.tree())
+    u = zd.zd_build(dev(pts), leaf_max=leaf_max)
+    for k in (10, 50):
+        gi, gd = gpu_knn_all(t, k)
+        ui, ud = gpu_knn_all(u, k)
+        assert np.array_equal(gi, ui) and np.array_equal(gd, ud)
+    q = zdgen.uniform(2000, 3, seed=86)
+    qi, qd = t.zd_knn(10, queries=dev(q))
+    torch.cuda.synchronize()
+    bi, bd = oracle_mod.brute_knn(pts, None, q, None, 10)
+    check_rows(qi.cpu().numpy(), qd.cpu().numpy(), bi, bd)
+    for m, seed in ((3, 87), (3000, 88)):   # a small (fast-path candidate) and a large batch
+        b = zdgen.points(dist, m, 3, seed=seed)
+        assert t.zd_insert(dev(b)) == live.insert(b)
+        assert_same_structure(t.zd_export(), live.tree())
+    kill = zdgen.delete_ids(12000, 4000, seed=89)
+    assert t.zd_delete(dev(kill)) == live.delete(kill)
+    assert_same_structure(t.zd_export(), live.tree())
+    oi, od, _ = live.tree().knn_all(10)
+    check_rows(*gpu_knn_all(t, 10), oi, od)
+
+
 def test_random_shift_errors(zd):
-    with pytest.raises(zd.ZdError) as e:
-        zd.zd_build(dev(zdgen.uniform(100, 3, seed=1)), shift=(1, 2, 3))
-    assert e.value.code == zd.ZD_EINVAL
+    for bad in ((-1, 0, 0), (0, 1 << 21, 0)):
+        with pytest.raises(zd.ZdError) as e:
+            zd.zd_build(dev(zdgen.uniform(100, 3, seed=1)), shift=bad)
+        assert e.value.code == zd.ZD_EINVAL
     for bad in ((-1, 0), (0, 1 << 30)):
         with pytest.raises(zd.ZdError) as e:
             zd.zd_build(dev(zdgen.uniform(100, 2, seed=1)), shift=bad)

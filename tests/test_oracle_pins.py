@@ -402,8 +402,9 @@ def test_random_shift_changes_the_tree(oracle_mod):
     pts = zdgen.uniform(4000, 2, seed=8)
     a, b = oracle_mod.Tree(pts), oracle_mod.Tree(pts, shift=(1 << 29, 12345))
     assert not np.array_equal(a.sorted_points()[1], b.sorted_points()[1])
-    with pytest.raises(ValueError):
-        oracle_mod.Tree(zdgen.uniform(10, 3, seed=1), shift=(1, 2, 3))
+    p3 = zdgen.uniform(4000, 3, seed=9)
+    a, b = oracle_mod.Tree(p3), oracle_mod.Tree(p3, shift=(1 << 20, 777, 3))
+    assert not np.array_equal(a.sorted_points()[1], b.sorted_points()[1])
 
 
 # ---- work counters -----------------------------------
@@ -446,3 +447,33 @@ def test_counters_match_appendix_a(oracle_mod, dim, app_a):
     assert per_q["replacements"] - per_q["evictions"] == pytest.approx(10.0)
     leaves = int((t.nodes()["split"] < 0).sum())
     assert abs(leaves / app_a["leaves"] - 1) < 0.01
+
+
+@pytest.mark.parametrize("dist", ["uniform", "plummer", "sphere"])
+@pytest.mark.parametrize("shift", [(0, 0, 0), (1, 2, 3), (2**21 - 1, 12345, 2**20)])
+def test_random_shift_3d_pins(oracle_mod, dist, shift):
+    """NEXT-4 random shift in 3D (Lemma 2.2; reading R31): shifted
+    coordinates take 22 bits; the key is the interleave of their levels 21..1 (63 bits,
+    checked by an independent big-int bit loop), the tree stays a valid zd-tree over
+    those keys, and the answer is the plain definition on the unshifted points."""
+    pts = zdgen.points(dist, 3000, 3, seed=15)
+    t = oracle_mod.Tree(pts, shift=shift)
+    check_tree_invariants(t)
+    keys, ids, coords = t.sorted_points()
+    sp = pts.astype(np.int64) + np.asarray(shift, np.int64)
+    assert np.array_equal(coords, sp[ids])
+    assert int(sp.max()) < 2**22
+    for j in range(0, len(ids), 89):
+        x, y, z = (int(v) for v in sp[ids[j]])
+        key = 0
+        for b in range(21, 0, -1):
+            key = (key << 3) | (((x >> b) & 1) << 2) | (((y >> b) & 1) << 1) | ((z >> b) & 1)
+        assert int(keys[j]) == key
+    rows = np.arange(len(pts), dtype=np.int32)
+    bi, bd = oracle_mod.brute_knn(pts, None, pts, rows, 10)
+    oi, od, _ = t.knn_all(10)
+    assert np.array_equal(oi, bi) and np.array_equal(od, bd)
+    q = zdgen.uniform(400, 3, seed=16)
+    qi, qd, _ = t.knn_queries(q, 7)
+    bqi, bqd = oracle_mod.brute_knn(pts, None, q, None, 7)
+    assert np.array_equal(qi, bqi) and np.array_equal(qd, bqd)
