@@ -261,7 +261,7 @@ class ZdTree:
 
 KNN_STATS = ("packets", "queries", "nodes", "pops", "ascents", "spans", "passes", "candidates", "hits",
              "rounds", "compactions", "survivors", "survivors_max", "cycles", "max_packet", "deferred") + tuple(f"hist{i}" for i in range(32)) + (
-    "insertions", "seed_hits", "seed_insertions", "seed_rounds", "lane_compactions")
+    "insertions", "seed_hits", "seed_insertions", "seed_rounds", "lane_compactions", "need_pairs", "raw_staged")
 
 
 def zd_knn_stats(reset: bool = True) -> dict:

@@ -134,7 +134,7 @@ void decr_apply(int dim, int64_t nb, const int32_t* del_before, int32_t* leaf_st
 // Work counters of the packet k-NN kernel (only in a -DZD_KNN_STATS build).
 enum { ZS_PACKETS = 0, ZS_QUERIES, ZS_NODES, ZS_POPS, ZS_ASCENTS, ZS_SPANS, ZS_PASSES, ZS_CAND, ZS_HITS,
        ZS_ROUNDS, ZS_COMPACT, ZS_SURV, ZS_SURV_MAX, ZS_CYCLES, ZS_MAXPKT, ZS_DEFERRED, ZS_HIST0, ZS_INS = ZS_HIST0 + 32,
-       ZS_SEED_HITS, ZS_SEED_INS, ZS_SEED_ROUNDS, ZS_LANE_COMPACT, ZD_NSTATS };
+       ZS_SEED_HITS, ZS_SEED_INS, ZS_SEED_ROUNDS, ZS_LANE_COMPACT, ZS_NEED_PAIRS, ZS_RAW, ZD_NSTATS };
 int knn_stats(unsigned long long* out, int n, int reset);
 void knn_all(const KnnArgs& a, cudaStream_t st);
 // External queries, already Morton-sorted (qkeys, qrecs with w = query index):

@@ -531,24 +531,27 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 if constexpr (DIM == 3) {
                     // 4 candidates per step: one 16-byte load per axis, packed f32x2
                     // arithmetic in the same order as the scalar test (dx^2, + dy^2, + dz^2)
-                    static_assert(ZD_SUB3 == 4, "packed test handles 4 candidates per step");
+                    static_assert(ZD_SUB3 == 4 || ZD_SUB3 == 8, "packed test: 4 or 8 candidates per step");
                     const float wb = L.wb;
                     const float2 qx = make_float2(L.qf[0], L.qf[0]), qy = make_float2(L.qf[1], L.qf[1]),
                                  qz = make_float2(L.qf[2], L.qf[2]);
 #pragma unroll 1
-                    for (int j0 = 0; j0 < CH; j0 += 4) {
+                    for (int j0 = 0; j0 < CH; j0 += ZD_SUB3) {
                         if (j0 >= cnt) break;
-                        const float4 X = *reinterpret_cast<const float4*>(&S.fx[h0 + j0]);
-                        const float4 Y = *reinterpret_cast<const float4*>(&S.fy[h0 + j0]);
-                        const float4 Z = *reinterpret_cast<const float4*>(&S.fz[h0 + j0]);
-                        const float2 dx0 = __fadd2_rn(qx, make_float2(-X.x, -X.y)), dx1 = __fadd2_rn(qx, make_float2(-X.z, -X.w));
-                        const float2 dy0 = __fadd2_rn(qy, make_float2(-Y.x, -Y.y)), dy1 = __fadd2_rn(qy, make_float2(-Y.z, -Y.w));
-                        const float2 dz0 = __fadd2_rn(qz, make_float2(-Z.x, -Z.y)), dz1 = __fadd2_rn(qz, make_float2(-Z.z, -Z.w));
-                        const float2 s0 = __ffma2_rn(dz0, dz0, __ffma2_rn(dy0, dy0, __fmul2_rn(dx0, dx0)));
-                        const float2 s1 = __ffma2_rn(dz1, dz1, __ffma2_rn(dy1, dy1, __fmul2_rn(dx1, dx1)));
-                        const uint32_t hb = (s0.x <= wb ? 1u : 0u) | (s0.y <= wb ? 2u : 0u) | (s1.x <= wb ? 4u : 0u) |
-                                            (s1.y <= wb ? 8u : 0u);
-                        hit |= hb << j0;
+#pragma unroll
+                        for (int j1 = j0; j1 < j0 + ZD_SUB3; j1 += 4) {
+                            const float4 X = *reinterpret_cast<const float4*>(&S.fx[h0 + j1]);
+                            const float4 Y = *reinterpret_cast<const float4*>(&S.fy[h0 + j1]);
+                            const float4 Z = *reinterpret_cast<const float4*>(&S.fz[h0 + j1]);
+                            const float2 dx0 = __fadd2_rn(qx, make_float2(-X.x, -X.y)), dx1 = __fadd2_rn(qx, make_float2(-X.z, -X.w));
+                            const float2 dy0 = __fadd2_rn(qy, make_float2(-Y.x, -Y.y)), dy1 = __fadd2_rn(qy, make_float2(-Y.z, -Y.w));
+                            const float2 dz0 = __fadd2_rn(qz, make_float2(-Z.x, -Z.y)), dz1 = __fadd2_rn(qz, make_float2(-Z.z, -Z.w));
+                            const float2 s0 = __ffma2_rn(dz0, dz0, __ffma2_rn(dy0, dy0, __fmul2_rn(dx0, dx0)));
+                            const float2 s1 = __ffma2_rn(dz1, dz1, __ffma2_rn(dy1, dy1, __fmul2_rn(dx1, dx1)));
+                            const uint32_t hb = (s0.x <= wb ? 1u : 0u) | (s0.y <= wb ? 2u : 0u) |
+                                                (s1.x <= wb ? 4u : 0u) | (s1.y <= wb ? 8u : 0u);
+                            hit |= hb << j1;
+                        }
                     }
                 } else {
                     const int64_t U = L.U;
@@ -640,6 +643,8 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
             {
                 ZD_STAT(ZS_CAND, cnt);
                 ZD_STAT(ZS_PASSES, 1);
+                ZD_STAT(ZS_NEED_PAIRS, w * cnt);   // pairs if only the needing lanes tested
+                ZD_STAT(ZS_RAW, n32r);
                 int hc = __popc(hit), hm = hc;
                 for (int o = 16; o > 0; o >>= 1) { hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o)); hc += __shfl_xor_sync(0xffffffffu, hc, o); }
                 ZD_STAT(ZS_HITS, hc);

@@ -325,7 +325,9 @@ void export_nodes(int dim, const void* nodes, const int32_t* split_bit, int64_t 
     else export_nodes_kernel<3><<<grid, 256, 0, st>>>((const Node<3>*)nodes, split_bit, nb, out);
 }
 
-size_t tree_blocks(int64_t n) { return (size_t)std::max<int64_t>(1, (n - 1 + TTILE - 1) / TTILE); }
+// blocks of the flags / compact kernels: they must cover every position (compact writes
+// pt_leaf of positions 0 .. n-1) as well as every pair 0 .. n-2
+size_t tree_blocks(int64_t n) { return (size_t)std::max<int64_t>(1, (n + TTILE - 1) / TTILE); }
 
 void topology_flags(const uint64_t* keys, int64_t n, int leaf_max, const TreeBufs& t, cudaStream_t st) {
     const size_t nblk = tree_blocks(n);

@@ -805,3 +805,17 @@ def test_knn_range_shards(zd, oracle_mod, parts):
         assert np.array_equal(oi.cpu().numpy(), ref_i) and np.array_equal(od.cpu().numpy(), ref_d)
     with pytest.raises(zd.ZdError):
         t.zd_knn_range(10, 5, n + 1, oi, od)
+
+
+@pytest.mark.parametrize("n", [1025, 2049, 4097, 10241])
+def test_pt_leaf_covers_every_position(zd, oracle_mod, n):
+    """Sizes with n - 1 a multiple of the topology tile (1024 pairs): the leaf of the
+    last sorted position is written too (it seeds the last k-NN packet)."""
+    pts = zdgen.uniform(n, 3, seed=n)
+    t = zd.zd_build(dev(pts))
+    ex = t.zd_export()
+    ls = ex["leaf_start"]
+    assert ls[-1] == n
+    gi, gd = gpu_knn_all(t, 10)
+    oi, od, _ = oracle_mod.Tree(pts).knn_all(10)
+    check_rows(gi, gd, oi, od)
