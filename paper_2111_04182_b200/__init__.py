@@ -138,6 +138,16 @@ def _as_i32(a):
     return a.contiguous()
 
 
+def _release_after(src, staged) -> None:
+    """If marshalling made a temporary CUDA copy of the caller's array (dtype or
+    layout conversion), wait for the device before the temporary can be freed: the
+    library may still be reading it on the tree's stream when the call returns (torch's
+    caching allocator would otherwise hand the memory to other work)."""
+    if staged is not src and not isinstance(staged, np.ndarray) and staged is not None and staged.is_cuda:
+        import torch
+        torch.cuda.synchronize(staged.device)
+
+
 def _current_stream() -> Optional[int]:
     try:
         import torch
@@ -196,6 +206,7 @@ class ZdTree:
             _check(load().zd_knn_ex(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2), flags))
         else:
             _check(load().zd_knn(self.handle, _ptr(q), m, k, _ptr(out_idx), _ptr(out_dist2)))
+        _release_after(queries, q)
         return out_idx, out_dist2
 
     def zd_knn_range(self, k: int, pos_lo: int, pos_hi: int, out_idx, out_dist2, root_based: bool = False,
@@ -209,11 +220,15 @@ class ZdTree:
 
     def zd_insert(self, batch) -> int:
         b = _as_i32(batch)
-        return _check(load().zd_insert(self.handle, _ptr(b), int(b.shape[0])))
+        r = _check(load().zd_insert(self.handle, _ptr(b), int(b.shape[0])))
+        _release_after(batch, b)
+        return r
 
     def zd_delete(self, ids) -> int:
         i = _as_i32(ids)
-        return _check(load().zd_delete(self.handle, _ptr(i), int(i.shape[0])))
+        r = _check(load().zd_delete(self.handle, _ptr(i), int(i.shape[0])))
+        _release_after(ids, i)
+        return r
 
     def zd_size(self) -> int:
         return _check(load().zd_size(self.handle))
@@ -310,6 +325,7 @@ def zd_build(points, dim: Optional[int] = None, leaf_max: int = 16, stream=None,
     sh = (C.c_int32 * 3)(*(list(shift) + [0] * (3 - len(shift)))) if shift is not None else (C.c_int32 * 3)()
     opts = _Opts(s, leaf_max, int(timing), int(shift is not None), sh)
     h = load().zd_build_ex(_ptr(p) if n else None, n, dim, C.byref(opts))
+    _release_after(points, p)
     if not h:
         raise ZdError(load().zd_last_error_code(), last_error())
     return ZdTree(h, dim)

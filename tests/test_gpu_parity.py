@@ -819,3 +819,25 @@ def test_pt_leaf_covers_every_position(zd, oracle_mod, n):
     gi, gd = gpu_knn_all(t, 10)
     oi, od, _ = oracle_mod.Tree(pts).knn_all(10)
     check_rows(gi, gd, oi, od)
+
+
+def test_converted_inputs(zd, oracle_mod):
+    """int64 / non-contiguous CUDA inputs are converted by the binding into temporaries
+    that stay alive until the device is done with them."""
+    base = zdgen.uniform(5000, 3, seed=91)
+    t = zd.zd_build(dev(base).to(torch.int64))
+    live = oracle_mod.LiveSet(base)
+    b = zdgen.uniform(4000, 3, seed=92)
+    wide = torch.zeros((4000, 6), dtype=torch.int32, device="cuda")
+    wide[:, ::2] = dev(b)
+    assert t.zd_insert(wide[:, ::2]) == live.insert(b)              # non-contiguous view
+    kill = zdgen.delete_ids(5000, 700, seed=93)
+    assert t.zd_delete(dev(kill).to(torch.int64)) == live.delete(kill)
+    q = zdgen.uniform(300, 3, seed=94)
+    qi, qd = t.zd_knn(5, queries=dev(q).to(torch.int64))
+    torch.cuda.synchronize()
+    ot = live.tree()
+    ei, ed, _ = ot.knn_queries(q, 5)
+    check_rows(qi.cpu().numpy(), qd.cpu().numpy(), ei, ed)
+    oi, od, _ = ot.knn_all(10)
+    check_rows(*gpu_knn_all(t, 10), oi, od)
