@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
                 // 3D shift: the key drops each coordinate's lowest bit, so the record
                 // comes from the input point (ids of a sort are id_base + input index)
                 const uint32_t id = s_ids[i];
+                ZD_DCHECK(id - id_base < n);
                 const int32_t* p = pts + (size_t)(id - id_base) * 3;
                 recs_out[dest] = make_int4(__ldg(p) + psh.x, __ldg(p + 1) + psh.y, __ldg(p + 2) + psh.z, (int)id);
             } else {
