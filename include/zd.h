@@ -200,6 +200,10 @@ typedef struct zd_info {
                              in the environment disables it) */
     int64_t fast_deletes; /* deletes applied without a topology rebuild (no leaf
                              emptied, every internal node kept > leaf_max points) */
+    int64_t sort_fallbacks; /* builds (n >= 2^20) whose truncated sort — 5 radix passes
+                             over key bits 24..63, then each run of equal 40-bit prefixes
+                             ranked by (key, id) — met a run longer than 64 and was
+                             redone with all 8 passes (degenerate, clustered inputs) */
 } zd_info;
 
 ZD_API int zd_get_info(const zd_tree *h, zd_info *out);

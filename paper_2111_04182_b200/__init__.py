@@ -45,7 +45,8 @@ class _Opts(C.Structure):
 class _Info(C.Structure):
     _fields_ = [("dim", C.c_int), ("leaf_max", C.c_int), ("n", C.c_int64), ("n_next", C.c_int64),
                 ("n_leaves", C.c_int64), ("n_internal", C.c_int64), ("root", C.c_int32),
-                ("node_words", C.c_int32), ("shift", C.c_int32 * 3), ("fast_inserts", C.c_int64), ("fast_deletes", C.c_int64)]
+                ("node_words", C.c_int32), ("shift", C.c_int32 * 3), ("fast_inserts", C.c_int64), ("fast_deletes", C.c_int64),
+                ("sort_fallbacks", C.c_int64)]
 
 
 def load():

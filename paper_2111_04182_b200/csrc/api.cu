@@ -183,6 +183,7 @@ struct zd_tree {
     int64_t ncap = 0;   // internal-node capacity of the node-indexed tree buffers
     int64_t fast_inserts = 0;   // inserts applied by the NEXT-2 fast path (introspection/tests)
     int64_t fast_deletes = 0;   // deletes applied by the NEXT-2 fast path
+    int64_t trunc_fallbacks = 0;   // builds whose truncated sort had to be redone with all passes
     bool shift_set = false;
     int32_t shift[3] = {0, 0, 0};   // random shift, applied before encoding
     // sorted live points
@@ -342,7 +343,7 @@ int ensure_id_cap(zd_tree* h, int64_t need) {
 // use_alt: the ping-pong buffers live in the idle update alternates keys2/recs2
 // (8 + 16 bytes per point = 2 x (u64 key + u32 id)); else they are allocated.
 int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
-              bool use_alt = false) {
+              bool use_alt = false, int* d_trunc_fail = nullptr) {
     if (n <= 0) return ZD_OK;
     Nvtx range("encode+radix sort");
     SortScratch s{};
@@ -361,7 +362,8 @@ int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint
     s.zero_words = sort_zero_words(n);
     ZD_CUDA(dalloc(&s.zero_block, s.zero_words, h->st));
     ZD_CUDA(dalloc(&s.offs, 8 * 256, h->st));
-    sort_points(h->dim, dpts, n, id_base, keys_out, recs_out, s, d_invalid(h), h->st, h->shift_set ? h->shift : nullptr);
+    sort_points(h->dim, dpts, n, id_base, keys_out, recs_out, s, d_invalid(h), h->st, h->shift_set ? h->shift : nullptr,
+                d_trunc_fail);
     ZD_CHECK_LAUNCH("sort_points");
     if (!alt) { dfree(s.k[0], h->st); dfree(s.k[1], h->st); dfree(s.v[0], h->st); dfree(s.v[1], h->st); }
     dfree(s.zero_block, h->st); dfree(s.offs, h->st);
@@ -375,6 +377,14 @@ void rec(zd_tree* h, int i) {
 void elapsed(zd_tree* h, int phase, int a, int b) {
     float t = 0.f;
     if (h->timing && cudaEventElapsedTime(&t, h->ev[a], h->ev[b]) == cudaSuccess) h->ms[phase] = t;
+}
+
+// Builds of at least this many points use the truncated sort (sort.cu); ZD_SORT_TRUNC=0
+// disables it (testing).
+constexpr int64_t kTruncSortMin = (int64_t)1 << 20;
+bool trunc_enabled() {
+    const char* e = std::getenv("ZD_SORT_TRUNC");
+    return !(e && e[0] == '0');
 }
 
 // Largest key count of one radix sort (sort.cu: 30-bit digit counts in the look-back
@@ -474,15 +484,29 @@ int do_build(zd_tree* h, const int32_t* points, int64_t n) {
     if ((rc = ensure_id_cap(h, std::max<int64_t>(n, 1)))) return rc;
     h->n = n;
     h->n_next = n;
+    // large builds sort with 5 passes + a run fixup; its verdict is read at the one sync
+    // (d_small[3]) and a failed fixup (runs of > 64 equal 40-bit prefixes: degenerate
+    // inputs) redoes the sort and topology with all 8 passes
+    const bool trunc = n >= kTruncSortMin && trunc_enabled();
     rec(h, 0);
-    if ((rc = sort_into(h, (const int32_t*)dpts, n, 0, h->keys, h->recs, true))) return rc;
+    if ((rc = sort_into(h, (const int32_t*)dpts, n, 0, h->keys, h->recs, true, trunc ? h->d_small + 3 : nullptr)))
+        return rc;
     rec(h, 1);
     if ((rc = topology(h))) return rc;
     rec(h, 2);
     set_alive_range(h->alive, 0, n, h->st);
     h->rows_identity = true;
-    if (owned) cudaFreeAsync(owned, h->st);
     if ((rc = refresh_host_meta(h))) return rc;   // the one sync: validation flag + node count
+    if (trunc && h->h_small[3] && !h->h_small[4]) {
+        h->trunc_fallbacks += 1;
+        rec(h, 0);
+        if ((rc = sort_into(h, (const int32_t*)dpts, n, 0, h->keys, h->recs, true))) return rc;
+        rec(h, 1);
+        if ((rc = topology(h))) return rc;
+        rec(h, 2);
+        if ((rc = refresh_host_meta(h))) return rc;
+    }
+    if (owned) cudaFreeAsync(owned, h->st);
     elapsed(h, PH_SORT, 0, 1);
     elapsed(h, PH_TOPO, 1, 6);
     elapsed(h, PH_BBOX, 6, 2);
@@ -947,6 +971,7 @@ int zd_get_info(const zd_tree* hc, zd_info* out) {
     for (int a = 0; a < 3; ++a) out->shift[a] = h->shift[a];
     out->fast_inserts = h->fast_inserts;
     out->fast_deletes = h->fast_deletes;
+    out->sort_fallbacks = h->trunc_fallbacks;
     return ZD_OK;
 }
 

@@ -53,9 +53,12 @@ size_t sort_zero_words(int64_t n);
 // shift2: the random shift (int32 [dim]) added after the range check, or NULL (2D:
 // 62-bit keys; 3D: keys of the shifted coordinates' levels 21..1, records gathered
 // from the input points).
+// d_trunc_fail != NULL: the truncated sort (5 passes + a rank fixup of equal-prefix
+// runs); *d_trunc_fail is set if a run was too long, and the caller must redo the sort
+// with d_trunc_fail == NULL (all 8 passes) before using the output.
 void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out,
                  int4* recs_out, const SortScratch& s, int* d_invalid, cudaStream_t st,
-                 const int32_t* shift2 = nullptr);
+                 const int32_t* shift2 = nullptr, int* d_trunc_fail = nullptr);
 
 // ---------------------------------------------------------------- tree (tree.cu)
 struct TreeBufs {

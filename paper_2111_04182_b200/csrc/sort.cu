@@ -260,9 +260,53 @@ __global__ void __launch_bounds__(ST, ZD_SORT_MINB) onesweep_kernel(
     (void)bad;
 }
 
+// Truncated sort (large builds): the LSD passes cover only the digits above bit
+// kTruncBits, leaving runs of keys that agree on bits >= kTruncBits in input (= id)
+// order; each element then finds its run and its rank in it by (key, id) and is
+// written to its final place, with its record.  Runs are short for real inputs (at 10M
+// 3D points the 39-bit prefix is shared by ~1 point on average, by ~4-10 at the
+// centre of the Plummer sphere); a run longer than kTruncRun sets *fail and the
+// caller redoes the sort with all 8 passes (checked at the build's one sync).
+constexpr int kTruncBits = 24;      // digits 3..7 sorted: 5 passes instead of 8
+constexpr uint32_t kTruncRun = 64;  // longest run resolved by the rank fixup
+template <int DIM>
+__global__ void __launch_bounds__(256) trunc_fixup_kernel(const uint64_t* __restrict__ keys_in,
+                                                          const uint32_t* __restrict__ ids_in, uint32_t n,
+                                                          uint64_t* __restrict__ keys_out, int4* __restrict__ recs_out,
+                                                          const int32_t* __restrict__ pts, uint32_t id_base, int4 psh,
+                                                          int* __restrict__ fail) {
+    const uint32_t i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t k = keys_in[i];
+    const uint32_t id = ids_in[i];
+    const uint64_t pre = k >> kTruncBits;
+    uint32_t lo = i, hi = i + 1;
+    while (lo > 0 && (__ldg(keys_in + lo - 1) >> kTruncBits) == pre) {
+        if (i - --lo >= kTruncRun) { atomicOr(fail, 1); return; }
+    }
+    while (hi < n && (__ldg(keys_in + hi) >> kTruncBits) == pre) {
+        if (++hi - i > kTruncRun) { atomicOr(fail, 1); return; }
+    }
+    uint32_t rank = 0;
+    for (uint32_t j = lo; j < hi; ++j) {
+        const uint64_t kj = __ldg(keys_in + j);
+        const uint32_t ij = __ldg(ids_in + j);
+        rank += (kj < k || (kj == k && ij < id)) ? 1u : 0u;   // ids are distinct: j == i never counts
+    }
+    const uint32_t dest = lo + rank;
+    ZD_DCHECK(dest < n);
+    keys_out[dest] = k;
+    if (DIM == 3 && psh.w == 3) {
+        const int32_t* p = pts + (size_t)(id - id_base) * 3;
+        recs_out[dest] = make_int4(__ldg(p) + psh.x, __ldg(p + 1) + psh.y, __ldg(p + 2) + psh.z, (int)id);
+    } else {
+        recs_out[dest] = decode_rec<DIM>(k, (int)id);
+    }
+}
+
 template <int DIM>
 void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
-                   const SortScratch& s, int* d_invalid, int4 psh, cudaStream_t st) {
+                   const SortScratch& s, int* d_invalid, int4 psh, cudaStream_t st, int* d_trunc_fail) {
     const uint32_t un = (uint32_t)n;
     const size_t tiles = sort_tiles(n);
     uint32_t* hist = s.zero_block;
@@ -287,6 +331,28 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
     hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid, psh, s.k[1]);
     scan_hist_kernel<<<1, 256, 0, st>>>(hist, s.offs);
     mark();
+    if (d_trunc_fail) {
+        // digits 3..7 (bits 24..63), then the rank fixup of equal-prefix runs
+        constexpr int P0 = kTruncBits / 8;
+        count_launch(2 + (NPASS - P0) + 1);
+        for (int p = P0; p < NPASS; ++p) {
+            const int q = p - P0;   // ping-pong index
+            uint32_t* stp = status + (size_t)p * tiles * 256;
+            const uint32_t* off = s.offs + p * 256;
+            if (q == 0)
+                onesweep_kernel<DIM, 0><<<tiles, ST, 0, st>>>(pts, s.k[1], nullptr, s.k[0], s.v[0], nullptr, un, 8 * p,
+                                                              id_base, off, stp, counters + p, psh);
+            else
+                onesweep_kernel<DIM, 1><<<tiles, ST, 0, st>>>(nullptr, s.k[(q - 1) & 1], s.v[(q - 1) & 1], s.k[q & 1],
+                                                              s.v[q & 1], nullptr, un, 8 * p, 0, off, stp, counters + p,
+                                                              psh);
+            mark();
+        }
+        const int qlast = NPASS - 1 - P0;
+        trunc_fixup_kernel<DIM><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+            s.k[qlast & 1], s.v[qlast & 1], un, keys_out, recs_out, pts, id_base, psh, d_trunc_fail);
+        mark();
+    } else {
     count_launch(2 + NPASS);
     for (int p = 0; p < NPASS; ++p) {
         uint32_t* stp = status + (size_t)p * tiles * 256;
@@ -302,6 +368,7 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
                                                           nullptr, recs_out, un, 8 * p, id_base, off, stp, counters + p,
                                                           psh);
         mark();
+    }
     }
     if (prof) {
         cudaEventSynchronize(pev[npev - 1]);
@@ -322,12 +389,12 @@ size_t sort_tiles(int64_t n) { return (size_t)((n + STILE - 1) / STILE); }
 size_t sort_zero_words(int64_t n) { return NPASS * 256 + NPASS + (size_t)NPASS * sort_tiles(n) * 256; }
 
 void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
-                 const SortScratch& s, int* d_invalid, cudaStream_t st, const int32_t* shift2) {
+                 const SortScratch& s, int* d_invalid, cudaStream_t st, const int32_t* shift2, int* d_trunc_fail) {
     if (n <= 0) return;
     const int4 psh = shift2 ? make_int4(shift2[0], shift2[1], dim == 3 ? shift2[2] : 0, dim)
                             : make_int4(0, 0, 0, 0);
-    if (dim == 2) sort_points_t<2>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st);
-    else sort_points_t<3>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st);
+    if (dim == 2) sort_points_t<2>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st, d_trunc_fail);
+    else sort_points_t<3>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st, d_trunc_fail);
 }
 
 }  // namespace zd

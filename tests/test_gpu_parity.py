@@ -841,3 +841,30 @@ def test_converted_inputs(zd, oracle_mod):
     check_rows(qi.cpu().numpy(), qd.cpu().numpy(), ei, ed)
     oi, od, _ = ot.knn_all(10)
     check_rows(*gpu_knn_all(t, 10), oi, od)
+
+
+@pytest.mark.parametrize("dist,dim,shift", [("uniform", 3, None), ("uniform", 2, None), ("plummer", 3, None),
+                                            ("sphere", 3, None), ("dup", 3, None), ("cube", 3, None),
+                                            ("uniform", 3, (12345, 1 << 20, 7)), ("cube", 3, (3, 5, 7))])
+def test_truncated_sort(zd, oracle_mod, monkeypatch, dist, dim, shift):
+    """Builds of >= 2^20 points sort with 5 radix passes (key bits 24..63) and rank each
+    run of equal 40-bit prefixes by (key, id); a run longer than 64 (here: every point
+    in a 2^8-cube, so all prefixes are equal) redoes the sort with all 8 passes.  Either
+    way the sorted arrays and the tree equal the full sort's and the oracle's."""
+    n = (1 << 20) + 3
+    if dist == "cube":
+        pts = (zdgen.uniform(n, 3, seed=97) >> 13).astype(np.int32)   # [0, 2^8)^3
+    else:
+        pts = zdgen.points(dist, n, dim, seed=96)
+    kw = {} if shift is None else dict(shift=shift)
+    t = zd.zd_build(dev(pts), **kw)
+    ex = t.zd_export()
+    assert ex["info"]["sort_fallbacks"] == (1 if dist in ("cube", "dup") else 0)   # dup: an 8^3 grid
+    monkeypatch.setenv("ZD_SORT_TRUNC", "0")
+    u = zd.zd_build(dev(pts), **kw)
+    ey = u.zd_export()
+    assert ey["info"]["sort_fallbacks"] == 0
+    assert np.array_equal(ex["keys"], ey["keys"]) and np.array_equal(ex["recs"], ey["recs"])
+    assert np.array_equal(ex["leaf_start"], ey["leaf_start"]) and np.array_equal(ex["nodes"], ey["nodes"])
+    if dist in ("uniform", "cube") and dim == 3 and shift is None:
+        assert_same_structure(ex, oracle_mod.Tree(pts))
