@@ -343,7 +343,7 @@ int ensure_id_cap(zd_tree* h, int64_t need) {
 // use_alt: the ping-pong buffers live in the idle update alternates keys2/recs2
 // (8 + 16 bytes per point = 2 x (u64 key + u32 id)); else they are allocated.
 int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
-              bool use_alt = false, int* d_trunc_fail = nullptr) {
+              bool use_alt = false, int* d_trunc_fail = nullptr, bool approx = false) {
     if (n <= 0) return ZD_OK;
     Nvtx range("encode+radix sort");
     SortScratch s{};
@@ -363,7 +363,7 @@ int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint
     ZD_CUDA(dalloc(&s.zero_block, s.zero_words, h->st));
     ZD_CUDA(dalloc(&s.offs, 8 * 256, h->st));
     sort_points(h->dim, dpts, n, id_base, keys_out, recs_out, s, d_invalid(h), h->st, h->shift_set ? h->shift : nullptr,
-                d_trunc_fail);
+                d_trunc_fail, approx);
     ZD_CHECK_LAUNCH("sort_points");
     if (!alt) { dfree(s.k[0], h->st); dfree(s.k[1], h->st); dfree(s.v[0], h->st); dfree(s.v[1], h->st); }
     dfree(s.zero_block, h->st); dfree(s.offs, h->st);
@@ -719,7 +719,9 @@ int knn_impl(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_
         ZD_CUDA(dalloc(&qr, m, h->st));
         ZD_CUDA(dalloc(&ql, m, h->st));
         if (ev0) cudaEventRecord(ev0, h->st);
-        if ((rc = sort_into(h, (const int32_t*)dq, m, 0, qk, qr))) return rc;
+        // the queries' order only serves locality (the answer does not depend on it):
+        // sort them by key bits 24..63 (5 passes)
+        if ((rc = sort_into(h, (const int32_t*)dq, m, 0, qk, qr, false, nullptr, true))) return rc;
         knn_queries(a, qk, qr, ql, m, h->st);
         ZD_CHECK_LAUNCH("knn_queries");
         if (ev1) cudaEventRecord(ev1, h->st);

@@ -55,10 +55,12 @@ size_t sort_zero_words(int64_t n);
 // from the input points).
 // d_trunc_fail != NULL: the truncated sort (5 passes + a rank fixup of equal-prefix
 // runs); *d_trunc_fail is set if a run was too long, and the caller must redo the sort
-// with d_trunc_fail == NULL (all 8 passes) before using the output.
+// with d_trunc_fail == NULL (all 8 passes) before using the output.  approx: order
+// by key bits 24..63 only (5 passes, no fixup) — for query batches, whose order only
+// serves locality.
 void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out,
                  int4* recs_out, const SortScratch& s, int* d_invalid, cudaStream_t st,
-                 const int32_t* shift2 = nullptr, int* d_trunc_fail = nullptr);
+                 const int32_t* shift2 = nullptr, int* d_trunc_fail = nullptr, bool approx = false);
 
 // ---------------------------------------------------------------- tree (tree.cu)
 struct TreeBufs {

@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(256) trunc_fixup_kernel(const uint64_t* __rest
 
 template <int DIM>
 void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
-                   const SortScratch& s, int* d_invalid, int4 psh, cudaStream_t st, int* d_trunc_fail) {
+                   const SortScratch& s, int* d_invalid, int4 psh, cudaStream_t st, int* d_trunc_fail, bool approx) {
     const uint32_t un = (uint32_t)n;
     const size_t tiles = sort_tiles(n);
     uint32_t* hist = s.zero_block;
@@ -331,7 +331,29 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
     hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid, psh, s.k[1]);
     scan_hist_kernel<<<1, 256, 0, st>>>(hist, s.offs);
     mark();
-    if (d_trunc_fail) {
+    if (approx) {
+        // order only by key bits 24..63 (digits 3..7); keys sharing those bits stay in
+        // input order — enough for the Morton locality of query batches
+        constexpr int P0 = kTruncBits / 8;
+        count_launch(2 + (NPASS - P0));
+        for (int p = P0; p < NPASS; ++p) {
+            const int q = p - P0;
+            uint32_t* stp = status + (size_t)p * tiles * 256;
+            const uint32_t* off = s.offs + p * 256;
+            if (q == 0)
+                onesweep_kernel<DIM, 0><<<tiles, ST, 0, st>>>(pts, s.k[1], nullptr, s.k[0], s.v[0], nullptr, un, 8 * p,
+                                                              id_base, off, stp, counters + p, psh);
+            else if (p < NPASS - 1)
+                onesweep_kernel<DIM, 1><<<tiles, ST, 0, st>>>(nullptr, s.k[(q - 1) & 1], s.v[(q - 1) & 1], s.k[q & 1],
+                                                              s.v[q & 1], nullptr, un, 8 * p, 0, off, stp, counters + p,
+                                                              psh);
+            else
+                onesweep_kernel<DIM, 2><<<tiles, ST, 0, st>>>(pts, s.k[(q - 1) & 1], s.v[(q - 1) & 1], keys_out,
+                                                              nullptr, recs_out, un, 8 * p, id_base, off, stp,
+                                                              counters + p, psh);
+            mark();
+        }
+    } else if (d_trunc_fail) {
         // digits 3..7 (bits 24..63), then the rank fixup of equal-prefix runs
         constexpr int P0 = kTruncBits / 8;
         count_launch(2 + (NPASS - P0) + 1);
@@ -389,12 +411,13 @@ size_t sort_tiles(int64_t n) { return (size_t)((n + STILE - 1) / STILE); }
 size_t sort_zero_words(int64_t n) { return NPASS * 256 + NPASS + (size_t)NPASS * sort_tiles(n) * 256; }
 
 void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
-                 const SortScratch& s, int* d_invalid, cudaStream_t st, const int32_t* shift2, int* d_trunc_fail) {
+                 const SortScratch& s, int* d_invalid, cudaStream_t st, const int32_t* shift2, int* d_trunc_fail,
+                 bool approx) {
     if (n <= 0) return;
     const int4 psh = shift2 ? make_int4(shift2[0], shift2[1], dim == 3 ? shift2[2] : 0, dim)
                             : make_int4(0, 0, 0, 0);
-    if (dim == 2) sort_points_t<2>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st, d_trunc_fail);
-    else sort_points_t<3>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st, d_trunc_fail);
+    if (dim == 2) sort_points_t<2>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st, d_trunc_fail, approx);
+    else sort_points_t<3>(pts, n, id_base, keys_out, recs_out, s, d_invalid, psh, st, d_trunc_fail, approx);
 }
 
 }  // namespace zd
