@@ -1221,19 +1221,41 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         if (lane == 0) atomicMax(&g_knn_stats[ZS_MAXPKT], ((unsigned long long)dt << 24) | (unsigned long long)(p0 >> 5));
     }
 #endif
-    KBest<K> best;
-    best.init();
-    for (int e = 0; e < L.cnt; ++e) {
-        const int4 c = __ldg(A.recs + S.be[e][lane].x);
-        const int64_t d = dist2<DIM>(L.q, c);
-        if (best.accepts(d, c.w)) best.insert(d, c.w);
-    }
     int32_t row = 0;
     if (active) {
         if (EXT) row = r.w;
         else row = A.row_of_id ? __ldg(A.row_of_id + r.w) : r.w;
     }
     if constexpr (ZD_COOP_OUT && 12 * K <= 8 * Cap<DIM, K>::v) {
+        // Exact (d2, id) order of the ~k survivors (reading 14): insertion sort of the
+        // lane's buffer column by a comparator that decides from the buffered upper
+        // bounds ub (d2 <= ub <= d2 (1 + 2^-20)) whenever they differ by more than that
+        // factor, and from the exact int64 d2 and id of both records otherwise.
+        const int cnt = L.cnt;
+        for (int e = 1; e < cnt; ++e) {
+            const int2 v = S.be[e][lane];
+            const float xv = __int_as_float(v.y), xv_hi = __fmul_ru(xv, 1.0f + 0x1p-19f);
+            int f = e - 1;
+            while (f >= 0) {
+                const int2 u = S.be[f][lane];
+                const float xu = __int_as_float(u.y);
+                bool before;   // v before u
+                if (xv_hi < xu) before = true;
+                else if (__fmul_ru(xu, 1.0f + 0x1p-19f) < xv) before = false;
+                else {
+                    const int4 cv = __ldg(A.recs + v.x), cu = __ldg(A.recs + u.x);
+                    const int64_t dv = dist2<DIM>(L.q, cv), du = dist2<DIM>(L.q, cu);
+                    before = dv < du || (dv == du && cv.w < cu.w);
+                }
+                if (!before) break;
+                S.be[f + 1][lane] = u;
+                --f;
+            }
+            S.be[f + 1][lane] = v;
+        }
+        int32_t pos[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) pos[t] = t < cnt ? S.be[t][lane].x : -1;
         // cooperative row writes: the packet's rows are staged in the (now idle) buffer
         // and written element-by-element by consecutive lanes, so one store covers ~3
         // rows instead of 32 scattered ones
@@ -1243,7 +1265,17 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
         int32_t* si = reinterpret_cast<int32_t*>(sd + 32 * K);
         __syncwarp();
 #pragma unroll
-        for (int t = 0; t < K; ++t) { sd[lane * K + t] = best.d[t]; si[lane * K + t] = best.i[t]; }
+        for (int t = 0; t < K; ++t) {
+            int64_t d = INT64_MAX;   // short rows are padded (reading 15)
+            int32_t id = -1;
+            if (pos[t] >= 0) {
+                const int4 c = __ldg(A.recs + pos[t]);
+                d = dist2<DIM>(L.q, c);
+                id = c.w;
+            }
+            sd[lane * K + t] = d;
+            si[lane * K + t] = id;
+        }
         S.p[lane] = active ? row : -1;
         __syncwarp();
 #pragma unroll 2
@@ -1255,12 +1287,21 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
                 A.out_d2[(int64_t)rw * A.k + ss] = sd[t];
             }
         }
-    } else if (active) {
-        int32_t* oi = A.out_idx + (int64_t)row * A.k;
-        int64_t* od = A.out_d2 + (int64_t)row * A.k;
+    } else {
+        KBest<K> best;
+        best.init();
+        for (int e = 0; e < L.cnt; ++e) {
+            const int4 c = __ldg(A.recs + S.be[e][lane].x);
+            const int64_t d = dist2<DIM>(L.q, c);
+            if (best.accepts(d, c.w)) best.insert(d, c.w);
+        }
+        if (active) {
+            int32_t* oi = A.out_idx + (int64_t)row * A.k;
+            int64_t* od = A.out_d2 + (int64_t)row * A.k;
 #pragma unroll
-        for (int s = 0; s < K; ++s) {
-            if (s < A.k) { oi[s] = best.i[s]; od[s] = best.d[s]; }
+            for (int s = 0; s < K; ++s) {
+                if (s < A.k) { oi[s] = best.i[s]; od[s] = best.d[s]; }
+            }
         }
     }
     return true;
