@@ -301,19 +301,28 @@ __device__ __forceinline__ void set_bound(Lane<DIM, K>& L) {
     }
 }
 
+// fp32 squared distance from q to the box (lo[3], hi[3]): per axis the gap
+// max(lo - q, q - hi, 0) (one 3-input max; exact, since lo <= hi and the coordinates
+// are exact in fp32), then dx^2, + dy^2, + dz^2 in the candidate test's order.
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+__device__ __forceinline__ float gap_d2(const float (&q)[3], const float* b) {
+    const float tx = fmax3(b[0] - q[0], q[0] - b[3], 0.f);
+    const float ty = fmax3(b[1] - q[1], q[1] - b[4], 0.f);
+    const float tz = fmax3(b[2] - q[2], q[2] - b[5], 0.f);
+    return fmaf(tz, tz, fmaf(ty, ty, tx * tx));
+}
+
 // Box distance in the lane's test domain: fp32 (3D) or exact int64 (2D).
 template <int DIM> struct BoxD { using T = int64_t; };
 template <> struct BoxD<3> { using T = float; };
 template <int DIM, int K>
 __device__ __forceinline__ typename BoxD<DIM>::T box_dist(const Lane<DIM, K>& L, const typename BoxT<DIM>::T* b) {
     if constexpr (DIM == 3) {
-        float df = 0.f;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const float t = fmaxf(b[a] - L.qf[a], 0.f) + fmaxf(L.qf[a] - b[3 + a], 0.f);
-            df = fmaf(t, t, df);
-        }
-        return df;
+        return gap_d2(L.qf, b);
     } else {
         return boxd2<DIM>(L.q, b);
     }
@@ -330,13 +339,7 @@ __device__ __forceinline__ bool within(const Lane<DIM, K>& L, typename BoxD<DIM>
 template <int DIM, int K>
 __device__ __forceinline__ bool box_need(const Lane<DIM, K>& L, const typename BoxT<DIM>::T* b) {
     if constexpr (DIM == 3) {
-        float df = 0.f;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const float t = fmaxf(b[a] - L.qf[a], 0.f) + fmaxf(L.qf[a] - b[3 + a], 0.f);
-            df = fmaf(t, t, df);
-        }
-        return df <= L.wb;
+        return gap_d2(L.qf, b) <= L.wb;
     } else {
         return boxd2<DIM>(L.q, b) <= L.U;
     }
@@ -481,9 +484,9 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 for (int g = 0; g < kPG; ++g) {
                     const float4 lo = S.pb[2 * g], hi = S.pb[2 * g + 1];
                     if constexpr (DIM == 3) {
-                        const float tx = fmaxf(lo.x - fc.x, 0.f) + fmaxf(fc.x - hi.x, 0.f);
-                        const float ty = fmaxf(lo.y - fc.y, 0.f) + fmaxf(fc.y - hi.y, 0.f);
-                        const float tz = fmaxf(lo.z - fc.z, 0.f) + fmaxf(fc.z - hi.z, 0.f);
+                        const float tx = fmax3(lo.x - fc.x, fc.x - hi.x, 0.f);
+                        const float ty = fmax3(lo.y - fc.y, fc.y - hi.y, 0.f);
+                        const float tz = fmax3(lo.z - fc.z, fc.z - hi.z, 0.f);
                         keep = keep || fmaf(tz, tz, fmaf(ty, ty, tx * tx)) <= gm[g];
                     } else {
                         const int tx = max(__float_as_int(lo.x) - r.x, 0) + max(r.x - __float_as_int(hi.x), 0);
