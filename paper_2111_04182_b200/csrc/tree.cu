@@ -153,6 +153,141 @@ __global__ void __launch_bounds__(TT) compact_kernel(const uint8_t* __restrict__
     }
 }
 
+// K4 in one pass (builds with node buffers sized for the worst case): the flags of
+// flags_kernel, the internal-node numbering of compact_kernel, with the tile's global
+// offset resolved by a decoupled look-back over the preceding tiles instead of a
+// separate block scan and a second read of the keys.  Tiles are taken in launch order
+// from a counter (every predecessor of a tile is resident or done).  Status words:
+// bits 31:30 = 1 aggregate / 2 inclusive prefix, bits 29:0 = the count (nb < n < 2^30).
+constexpr uint32_t kTopoVal = (1u << 30) - 1, kTopoAgg = 1u << 30, kTopoInc = 2u << 30;
+#ifndef ZD_TOPO_TPI
+#define ZD_TOPO_TPI 8
+#endif
+constexpr int TPI2 = ZD_TOPO_TPI;      // pairs per thread in topo_kernel
+constexpr int TTILE2 = TT * TPI2;      // pairs per topo_kernel tile
+static_assert(TPI2 % 4 == 0, "topo_kernel stores a thread's pt_leaf entries as int4s");
+
+__global__ void __launch_bounds__(TT) topo_kernel(const uint64_t* __restrict__ keys, uint32_t n, int leaf_max,
+                                                  uint32_t* status, uint32_t ntiles, int32_t* __restrict__ split_bit,
+                                                  int32_t* __restrict__ leaf_start, int32_t* __restrict__ pt_leaf,
+                                                  int32_t* __restrict__ meta, uint32_t* __restrict__ visit,
+                                                  int32_t* __restrict__ node_words, int nw) {
+    __shared__ __align__(16) uint8_t s_delta[TTILE2 + 2 * HALO + 8];   // delta + 1; 128 = boundary
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_tile, s_excl;
+    uint32_t* counter = status + ntiles;
+    if (threadIdx.x == 0) {
+        const uint32_t t = atomicAdd(counter, 1u);
+        s_tile = t;
+    }
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t base = (int64_t)tile * TTILE2;
+    const int64_t npairs = (int64_t)n - 1;
+    for (int t = threadIdx.x; t < TTILE2 + 2 * HALO; t += TT) {
+        const int64_t p = base - HALO + t;
+        s_delta[t] = (p >= 0 && p < npairs) ? (uint8_t)(delta_of(keys[p], keys[p + 1]) + 1) : (uint8_t)128;
+    }
+    __syncthreads();
+    const int W = leaf_max - 1;
+    uint8_t f[TPI2];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < TPI2; ++i) {
+        const int off = threadIdx.x * TPI2 + i;   // blocked: a thread's pairs are consecutive
+        const int64_t p = base + off;
+        const int c = HALO + off;
+        const int d = s_delta[c];   // delta + 1
+        bool big = false;
+        if (p < npairs && d >= 1) {
+            int l = 1, r = 1;
+            if (W <= 15) {
+                const uint32_t gl = greater_mask16(s_delta, c - 16, d);
+                const uint32_t gr = greater_mask16(s_delta, c + 1, d);
+                const uint32_t ml = gl & (0xffffu << (16 - W));
+                const uint32_t mr = gr & ((1u << W) - 1u);
+                l = ml ? 16 - (31 - __clz(ml)) : W + 1;
+                r = mr ? __ffs(mr) : W + 1;
+            } else {
+                while (l <= W && s_delta[c - l] <= d) ++l;
+                while (r <= W && s_delta[c + r] <= d) ++r;
+            }
+            big = (l + r) > leaf_max;
+        }
+        f[i] = big;
+        cnt += big;
+    }
+    uint32_t total;
+    const uint32_t local = block_exclusive_scan<TT>(cnt, s_warp, &total);
+    // decoupled look-back: one warp folds the predecessors' words 32 at a time
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        uint32_t* mine = status + tile;
+        if (lane == 0) {
+            cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(*mine).store(
+                (tile == 0 ? kTopoInc : kTopoAgg) | total, cuda::memory_order_relaxed);
+        }
+        uint32_t excl = 0;
+        int64_t t = (int64_t)tile - 1;
+        while (t >= 0) {
+            const int64_t q = t - lane;
+            uint32_t v = kTopoInc;   // past tile 0: an inclusive zero
+            if (q >= 0) {
+                do {
+                    v = cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(status[q]).load(cuda::memory_order_relaxed);
+                } while ((v & ~kTopoVal) == 0);
+            }
+            const uint32_t inc = __ballot_sync(0xffffffffu, (v & ~kTopoVal) == kTopoInc);
+            const int stop = inc ? __ffs(inc) - 1 : 31;   // nearest inclusive predecessor in the window
+            uint32_t x = lane <= stop ? (v & kTopoVal) : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            excl += x;
+            if (inc) break;
+            t -= 32;
+        }
+        if (lane == 0) {
+            if (tile > 0)
+                cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(*mine).store(kTopoInc | (excl + total),
+                                                                                   cuda::memory_order_relaxed);
+            s_excl = excl;
+            if (tile == ntiles - 1) {
+                const uint32_t nb = excl + total;
+                meta[0] = (int32_t)nb;
+                meta[1] = nb == 0 ? ~0 : -1;   // root: single leaf, or set by the bottom-up pass
+                leaf_start[0] = 0;
+                leaf_start[nb + 1] = (int32_t)n;
+                *counter = 0;                  // every tile id is taken: reset for the next build
+            }
+        }
+    }
+    __syncthreads();
+    uint32_t run = s_excl + local;
+    const int64_t p0 = base + threadIdx.x * TPI2;
+    int32_t pl[TPI2];
+#pragma unroll
+    for (int i = 0; i < TPI2; ++i) {
+        const int64_t p = p0 + i;
+        pl[i] = (int32_t)run;   // leaf = number of big pairs before p
+        if (f[i]) {
+            split_bit[run] = s_delta[HALO + threadIdx.x * TPI2 + i] - 1;
+            leaf_start[run + 1] = (int32_t)(p + 1);
+            node_words[(size_t)run * nw + nw - 1] = (int32_t)(p + 1);   // Node::mid
+            visit[run] = 0u;
+            ++run;
+        }
+    }
+    if (p0 + TPI2 <= (int64_t)n) {
+#pragma unroll
+        for (int i = 0; i < TPI2; i += 4)
+            *reinterpret_cast<int4*>(pt_leaf + p0 + i) = make_int4(pl[i], pl[i + 1], pl[i + 2], pl[i + 3]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < TPI2; ++i)
+            if (p0 + i < (int64_t)n) pt_leaf[p0 + i] = pl[i];
+    }
+}
+
 template <int DIM>
 __device__ __forceinline__ void store_box(typename BoxT<DIM>::T* dst, const int32_t (&b)[2 * DIM]) {
 #pragma unroll
@@ -362,8 +497,16 @@ void build_topology(int dim, const uint64_t* keys, const int4* recs, int64_t n, 
         if (ev_mid) cudaEventRecord(ev_mid, st);
         topology_boxes(dim, recs, n, t, st);
     } else {
-        topology_flags(keys, n, leaf_max, t, st);
-        topology_finish(dim, keys, recs, n, t, st, ev_mid);
+        // one pass: flags + look-back numbering (status words and the tile counter live
+        // in block_cnt, zeroed here)
+        const uint32_t ntiles = (uint32_t)((n + TTILE2 - 1) / TTILE2);
+        cudaMemsetAsync(t.block_cnt, 0, (ntiles + 1) * sizeof(uint32_t), st);
+        const int nw = dim == 2 ? (int)(sizeof(Node<2>) / 4) : (int)(sizeof(Node<3>) / 4);
+        topo_kernel<<<ntiles, TT, 0, st>>>(keys, un, leaf_max, t.block_cnt, ntiles, t.split_bit, t.leaf_start, t.pt_leaf,
+                                           t.d_meta, t.visit, (int32_t*)t.nodes, nw);
+        count_launch(1);
+        if (ev_mid) cudaEventRecord(ev_mid, st);
+        topology_boxes(dim, recs, n, t, st);
     }
 }
 
