@@ -288,10 +288,18 @@ __global__ void __launch_bounds__(TT) topo_kernel(const uint64_t* __restrict__ k
     }
 }
 
+// a child box into its parent node: vector stores (3D: fp32 pairs at 8-byte offsets;
+// 2D: one int4 at a 16-byte offset); the conversion is exact (3D: < 2^21)
 template <int DIM>
 __device__ __forceinline__ void store_box(typename BoxT<DIM>::T* dst, const int32_t (&b)[2 * DIM]) {
-#pragma unroll
-    for (int a = 0; a < 2 * DIM; ++a) dst[a] = (typename BoxT<DIM>::T)b[a];   // exact (3D: < 2^21)
+    if constexpr (DIM == 3) {
+        float2* d = reinterpret_cast<float2*>(dst);
+        d[0] = make_float2((float)b[0], (float)b[1]);
+        d[1] = make_float2((float)b[2], (float)b[3]);
+        d[2] = make_float2((float)b[4], (float)b[5]);
+    } else {
+        *reinterpret_cast<int4*>(dst) = make_int4(b[0], b[1], b[2], b[3]);
+    }
 }
 
 // One block per window of BW consecutive leaves.  An internal node whose whole leaf
@@ -393,10 +401,11 @@ __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ 
             Node<DIM>* P = nodes + par;
             // a leaf child is encoded by its point range: left = ~start, right = ~end
             const int32_t cref = ref >= 0 ? ref : (as_right ? ~e : ~s);
-            if (as_right) { store_box<DIM>(P->rbox, bb); P->right = cref; range[2 * par + 1] = R; }
-            else { store_box<DIM>(P->lbox, bb); P->left = cref; range[2 * par] = L; }
-            if (ref < 0) leaf_parent[l] = par; else nodes[ref].parent = par;
             const bool loc = par >= b0 && par < b0 + BW && s_local[par - b0];
+            if (as_right) { store_box<DIM>(P->rbox, bb); P->right = cref; }
+            else { store_box<DIM>(P->lbox, bb); P->left = cref; }
+            range[2 * par + (as_right ? 1 : 0)] = as_right ? R : L;   // leaf bounds (also read by the delete check)
+            if (ref < 0) leaf_parent[l] = par; else nodes[ref].parent = par;
             if (loc) {
                 // both children of par finish in this block: exchange through shared
                 // memory with a block-scoped release/acquire
