@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ 
     __shared__ uint8_t s_local[BW];       // node b0+t finishes inside this block
     __shared__ uint32_t s_visit[BW];      // block-local arrival counters
     __shared__ int32_t s_rng[BW][2];      // block-local nodes: children's leaf bounds (L of left, R of right)
-    __shared__ int32_t s_box[BW][2][2 * DIM];   // block-local nodes: children's boxes
+    __shared__ __align__(8) int32_t s_box[BW][2][2 * DIM];   // block-local nodes: children's boxes
     const int32_t nb = meta[0];
     const int32_t b0 = blockIdx.x * BW;
     if (b0 > nb) return;                  // block-uniform
@@ -411,15 +411,23 @@ __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ 
                 // memory with a block-scoped release/acquire
                 const int pi = par - b0, side = as_right ? 1 : 0;
 #pragma unroll
-                for (int a = 0; a < 2 * DIM; ++a) s_box[pi][side][a] = bb[a];
+                for (int a = 0; a < DIM; ++a)
+                    reinterpret_cast<int2*>(s_box[pi][side])[a] = make_int2(bb[2 * a], bb[2 * a + 1]);
                 s_rng[pi][side] = as_right ? R : L;
                 __threadfence_block();
                 if (atomicAdd(&s_visit[pi], 1u) == 0) break;
                 __threadfence_block();
+                int32_t ob[2 * DIM];
 #pragma unroll
                 for (int a = 0; a < DIM; ++a) {
-                    bb[a] = min(bb[a], s_box[pi][side ^ 1][a]);
-                    bb[DIM + a] = max(bb[DIM + a], s_box[pi][side ^ 1][DIM + a]);
+                    const int2 v = reinterpret_cast<const int2*>(s_box[pi][side ^ 1])[a];
+                    ob[2 * a] = v.x;
+                    ob[2 * a + 1] = v.y;
+                }
+#pragma unroll
+                for (int a = 0; a < DIM; ++a) {
+                    bb[a] = min(bb[a], ob[a]);
+                    bb[DIM + a] = max(bb[DIM + a], ob[DIM + a]);
                 }
                 if (as_right) L = s_rng[pi][0]; else R = s_rng[pi][1];
             } else {
