@@ -1,5 +1,5 @@
 """Per-CUDA-line instruction and stall-sample shares from an ncu report's mixed
-source view (dev aid): python scripts/ncu_lines.py report.ncu-rep [top]"""
+source view (dev aid): python scripts/ncu_lines.py report.ncu-rep [top] [kernel regex]"""
 import csv
 import io
 import subprocess
@@ -7,7 +7,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 60
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+kfilt = ["--kernel-name", f"regex:{sys.argv[3]}", "--launch-count", "1"] if len(sys.argv) > 3 else []
+out = subprocess.run(["ncu", "-i", rep, *kfilt, "--page", "source", "--csv", "--print-source=cuda,sass"],
                      capture_output=True, text=True).stdout
 fname = "?"
 hdr = None
