@@ -662,7 +662,7 @@ int knn_impl(zd_tree* h, const int32_t* queries, int64_t m, int k, int32_t* out_
     constexpr int kHardCap = 1 << 15;
     int32_t* hard = nullptr;
     ZD_CUDA(dalloc(&hard, kHardCap + 2, h->st));
-    ZD_CUDA(cudaMemsetAsync(hard, 0, sizeof(int32_t), h->st));
+    ZD_CUDA(cudaMemsetAsync(hard, 0, 2 * sizeof(int32_t), h->st));   // [0] deferred count, [1] packet counter
     KnnArgs a{};
     a.hard_count = hard;
     a.hard_list = hard + 2;

@@ -106,7 +106,7 @@ struct KnnArgs {
     int32_t* out_idx;
     int64_t* out_d2;
     int32_t* hard_list;          // [hard_cap] scratch for deferred packets (NULL: none)
-    int32_t* hard_count;         // zeroed by the caller
+    int32_t* hard_count;         // [0] deferred packets, [1] persistent packet counter: zeroed by the caller
     int hard_cap;
     int defer_all;               // testing: every packet goes to the second pass
     int root_based;              // ablation: root-based search

@@ -35,6 +35,7 @@
 // a superset of what its own searchUp would see and drops a point only by its own
 // sound rules; the (d2, id) order makes the answer unique.  Self is excluded by id
 // (reading 13); short rows are padded with (-1, INT64_MAX) (reading 15).
+#include <algorithm>
 #include <climits>
 #include <cstddef>
 
@@ -976,13 +977,16 @@ struct PacketArgs {
     int32_t* out_idx;
     int64_t* out_d2;
     int32_t* hard_list;        // packets deferred to the second pass (NULL: never defer)
-    int32_t* hard_count;
+    int32_t* hard_count;       // [0] deferred packets, [1] next packet of the persistent first pass
     int hard_cap;
     int hard_mode;             // 0: packets; 1: second pass over the deferred packets' queries
     int defer_all;             // testing: defer every packet (hard_list must be set)
     int root_based;            // ablation: root-based search instead of leaf-based
 };
 
+#ifndef ZD_PERSIST
+#define ZD_PERSIST 1     // persistent first pass (needs hard_count[1] zeroed; grid = resident blocks)
+#endif
 #ifndef ZD_INCOHERENT
 #define ZD_INCOHERENT 4096.0f   // defer a packet if its extent^2 > this * median bound
 #endif
@@ -1328,10 +1332,27 @@ __global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? (DIM == 3 ? ZD_MINB3
     const int64_t gw = (int64_t)blockIdx.x * Pw<K>::v + wib;
     const int64_t qe = (int64_t)A.q_lo + A.nq;   // queries are the positions [q_lo, qe)
     if (!A.hard_mode) {
+#if ZD_PERSIST
+        // persistent warps: packets are taken in Morton order from a counter, so a warp
+        // that finishes early starts the next packet instead of idling until its block's
+        // slowest warp is done
+        const int64_t npk = ((int64_t)A.nq + 31) / 32;
+        (void)gw;
+        while (true) {
+            int64_t pk = 0;
+            if (lane == 0) pk = atomicAdd(reinterpret_cast<unsigned int*>(A.hard_count + 1), 1u);
+            pk = __shfl_sync(0xffffffffu, pk, 0);
+            if (pk >= npk) break;
+            const int64_t p0 = A.q_lo + pk * 32;
+            const int32_t pe = (int32_t)(p0 + 32 < qe ? p0 + 32 : qe);
+            search_packet<DIM, K, EXT>(A, (int32_t)p0, pe, pk, A.hard_list != nullptr, S, lane);
+        }
+#else
         if (gw * 32 >= A.nq) return;   // whole warp exits together
         const int64_t p0 = A.q_lo + gw * 32;
         const int32_t pe = (int32_t)(p0 + 32 < qe ? p0 + 32 : qe);
         search_packet<DIM, K, EXT>(A, (int32_t)p0, pe, gw, A.hard_list != nullptr, S, lane);
+#endif
     } else {
         // second pass: the deferred packets' queries, one per warp (grid-stride)
         const int64_t cnt = min(*A.hard_count, A.hard_cap);
@@ -1378,13 +1399,26 @@ PacketArgs packet_args(const KnnArgs& a) {
 template <int DIM, int K, bool EXT>
 void launch_packets(const PacketArgs& A, cudaStream_t st) {
     const int64_t warps = ((int64_t)A.nq + 31) / 32;
-    const int grid = (int)((warps + Pw<K>::v - 1) / Pw<K>::v);
+    int grid = (int)((warps + Pw<K>::v - 1) / Pw<K>::v);
     if (grid <= 0) return;
     const size_t smem = sizeof(WarpSh<DIM, K>) * Pw<K>::v;
     static PerDeviceOnce attr;   // per template instance and device (concurrent zd_knn calls)
-    attr.run([&](int) {
+    static int resident[64];     // per device: SMs x resident blocks of this instance
+    attr.run([&](int dev) {
         cudaFuncSetAttribute(knn_packet_kernel<DIM, K, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int sms = 148, per = 1;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, knn_packet_kernel<DIM, K, EXT>, Pw<K>::v * 32, smem);
+        if (dev >= 0 && dev < 64) resident[dev] = sms * (per > 0 ? per : 1);
     });
+#if ZD_PERSIST
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const int r = (dev >= 0 && dev < 64 && resident[dev] > 0) ? resident[dev] : 148 * 8;
+        grid = std::min(grid, r);
+    }
+#endif
     count_launch(1);
     knn_packet_kernel<DIM, K, EXT><<<grid, Pw<K>::v * 32, smem, st>>>(A);
     if (A.hard_list) {
