@@ -987,6 +987,9 @@ struct PacketArgs {
 #ifndef ZD_PERSIST
 #define ZD_PERSIST 1     // persistent first pass (needs hard_count[1] zeroed; grid = resident blocks)
 #endif
+#ifndef ZD_PCHUNK
+#define ZD_PCHUNK 1      // packets per fetch of a persistent warp
+#endif
 #ifndef ZD_INCOHERENT
 #define ZD_INCOHERENT 4096.0f   // defer a packet if its extent^2 > this * median bound
 #endif
@@ -1338,14 +1341,21 @@ __global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? (DIM == 3 ? ZD_MINB3
         // slowest warp is done
         const int64_t npk = ((int64_t)A.nq + 31) / 32;
         (void)gw;
+        // a fetch takes ZD_PCHUNK consecutive packets, searched one after the other
+        int64_t pk = 0, pk_end = 0;
         while (true) {
-            int64_t pk = 0;
-            if (lane == 0) pk = atomicAdd(reinterpret_cast<unsigned int*>(A.hard_count + 1), 1u);
-            pk = __shfl_sync(0xffffffffu, pk, 0);
-            if (pk >= npk) break;
+            if (pk == pk_end) {
+                int64_t c = 0;
+                if (lane == 0) c = atomicAdd(reinterpret_cast<unsigned int*>(A.hard_count + 1), 1u);
+                c = __shfl_sync(0xffffffffu, c, 0);
+                pk = c * ZD_PCHUNK;
+                if (pk >= npk) break;
+                pk_end = min(pk + ZD_PCHUNK, npk);
+            }
             const int64_t p0 = A.q_lo + pk * 32;
             const int32_t pe = (int32_t)(p0 + 32 < qe ? p0 + 32 : qe);
             search_packet<DIM, K, EXT>(A, (int32_t)p0, pe, pk, A.hard_list != nullptr, S, lane);
+            ++pk;
         }
 #else
         if (gw * 32 >= A.nq) return;   // whole warp exits together
