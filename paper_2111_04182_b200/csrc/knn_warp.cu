@@ -22,6 +22,8 @@
 // k written; short rows are padded with (-1, INT64_MAX) (reading 15).
 #include <climits>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -59,6 +61,7 @@ struct KwArgs {
     int32_t* out_idx;
     int64_t* out_d2;
     int ext, root_based;
+    unsigned int* next;        // persistent warps: next query (zeroed by the caller)
 };
 
 struct Sub {
@@ -401,13 +404,9 @@ __device__ __forceinline__ void kw_down(const KwArgs& A, const Node<DIM>* __rest
     }
 }
 
+// one query (Morton position qi) searched by the whole warp
 template <int DIM>
-__global__ void __launch_bounds__(KW_WARPS * 32, ZD_KW_MINB) knn_warp_kernel(KwArgs A) {
-    __shared__ KwSh sh[KW_WARPS];
-    const int lane = threadIdx.x & 31;
-    KwSh& S = sh[threadIdx.x >> 5];
-    const int64_t qi = (int64_t)blockIdx.x * KW_WARPS + (threadIdx.x >> 5);
-    if (qi >= A.nq) return;   // whole warp
+__device__ __forceinline__ void kw_query(const KwArgs& A, int64_t qi, KwSh& S, int lane) {
     const Node<DIM>* nodes = static_cast<const Node<DIM>*>(A.nodes);
     const int4 r = __ldg(A.qrecs + qi);
     KwQuery<DIM> q;
@@ -480,6 +479,23 @@ __global__ void __launch_bounds__(KW_WARPS * 32, ZD_KW_MINB) knn_warp_kernel(KwA
     }
 }
 
+// Persistent warps: each takes the next query in Morton order from a counter (a warp
+// that finishes early starts another query instead of idling until its block is done).
+template <int DIM>
+__global__ void __launch_bounds__(KW_WARPS * 32, ZD_KW_MINB) knn_warp_kernel(KwArgs A) {
+    __shared__ KwSh sh[KW_WARPS];
+    const int lane = threadIdx.x & 31;
+    KwSh& S = sh[threadIdx.x >> 5];
+    while (true) {
+        int64_t qi = 0;
+        if (lane == 0) qi = atomicAdd(A.next, 1u);
+        qi = __shfl_sync(0xffffffffu, qi, 0);
+        if (qi >= A.nq) break;   // whole warp
+        kw_query<DIM>(A, qi, S, lane);
+        __syncwarp();
+    }
+}
+
 }  // namespace
 
 void knn_warp(const KnnArgs& a, const int4* qrecs, const int32_t* qleaf, int64_t nq, bool ext, cudaStream_t st) {
@@ -489,7 +505,24 @@ void knn_warp(const KnnArgs& a, const int4* qrecs, const int32_t* qleaf, int64_t
     A.pos_range = a.pos_range; A.d_meta = a.d_meta; A.qrecs = qrecs; A.qleaf = qleaf;
     A.nq = (int32_t)nq; A.n_pts = (int32_t)a.n; A.k = a.k; A.row_of_id = ext ? nullptr : a.row_of_id;
     A.out_idx = a.out_idx; A.out_d2 = a.out_d2; A.ext = ext ? 1 : 0; A.root_based = a.root_based;
-    const int grid = (int)((nq + KW_WARPS - 1) / KW_WARPS);
+    A.next = reinterpret_cast<unsigned int*>(a.hard_count + 1);   // zeroed by zd_knn
+    int grid = (int)((nq + KW_WARPS - 1) / KW_WARPS);
+    static PerDeviceOnce occ;
+    static int resident[2][64];   // per dimension and device: SMs x resident blocks
+    occ.run([&](int dev) {
+        int sms = 148, p2 = 1, p3 = 1;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, knn_warp_kernel<2>, KW_WARPS * 32, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p3, knn_warp_kernel<3>, KW_WARPS * 32, 0);
+        if (dev >= 0 && dev < 64) {
+            resident[0][dev] = sms * (p2 > 0 ? p2 : 1);
+            resident[1][dev] = sms * (p3 > 0 ? p3 : 1);
+        }
+    });
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int r = (dev >= 0 && dev < 64) ? resident[a.dim == 3][dev] : 0;
+    if (r > 0) grid = std::min(grid, r);
     count_launch(1);
     if (a.dim == 2) knn_warp_kernel<2><<<grid, KW_WARPS * 32, 0, st>>>(A);
     else knn_warp_kernel<3><<<grid, KW_WARPS * 32, 0, st>>>(A);
