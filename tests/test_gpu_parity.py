@@ -30,7 +30,9 @@ def check_rows(gi, gd, oi, od):
 
 
 # one-sweep tiles of 13 x 256 = 3328 keys
-SIZES = [0, 1, 2, 3, 16, 17, 33, 1000, 2047, 2048, 2049, 2815, 2816, 2817, 3327, 3328, 3329, 6657, 20011]
+# sort tiles of 3328 keys, one-pass topology tiles of 2048 pairs (n - 1 pairs)
+SIZES = [0, 1, 2, 3, 16, 17, 33, 1000, 2047, 2048, 2049, 2050, 2815, 2816, 2817, 3327, 3328, 3329, 4097, 4098,
+         6145, 6657, 20011]
 
 
 @pytest.mark.parametrize("n", SIZES)
