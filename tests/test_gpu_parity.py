@@ -1,6 +1,6 @@
 """GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
 
-Sizes span several sort tiles (3328 keys), several topology blocks (1024 pairs) and
+Sizes span several sort tiles (3328 keys), several topology tiles (2048 pairs) and
 ragged tails; edge cases cover empty / single / duplicate-heavy inputs, every k
 template and leaf sizes 1..32.
 """
@@ -29,7 +29,6 @@ def check_rows(gi, gd, oi, od):
     assert bad.size == 0, f"{bad.size} rows differ, first row {bad[0]}: gpu {gi[bad[0]]} {gd[bad[0]]} oracle {oi[bad[0]]} {od[bad[0]]}"
 
 
-# one-sweep tiles of 13 x 256 = 3328 keys
 # sort tiles of 3328 keys, one-pass topology tiles of 2048 pairs (n - 1 pairs)
 SIZES = [0, 1, 2, 3, 16, 17, 33, 1000, 2047, 2048, 2049, 2050, 2815, 2816, 2817, 3327, 3328, 3329, 4097, 4098,
          6145, 6657, 20011]
