@@ -346,6 +346,12 @@ int sort_into(zd_tree* h, const int32_t* dpts, int64_t n, uint32_t id_base, uint
               bool use_alt = false, int* d_trunc_fail = nullptr, bool approx = false) {
     if (n <= 0) return ZD_OK;
     Nvtx range("encode+radix sort");
+    if (n <= kSmallSort) {   // small batches: one rank-by-counting launch (sort.cu)
+        sort_points_small(h->dim, dpts, n, id_base, keys_out, recs_out, d_invalid(h), h->st,
+                          h->shift_set ? h->shift : nullptr);
+        ZD_CHECK_LAUNCH("sort_points_small");
+        return ZD_OK;
+    }
     SortScratch s{};
     const bool alt = use_alt && h->keys2 && h->recs2 && n <= h->cap;
     if (alt) {

@@ -61,6 +61,10 @@ size_t sort_zero_words(int64_t n);
 void sort_points(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out,
                  int4* recs_out, const SortScratch& s, int* d_invalid, cudaStream_t st,
                  const int32_t* shift2 = nullptr, int* d_trunc_fail = nullptr, bool approx = false);
+// The same order for n <= kSmallSort keys in one single-block launch (no scratch).
+constexpr int kSmallSort = 256;
+void sort_points_small(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
+                       int* d_invalid, cudaStream_t st, const int32_t* shift2 = nullptr);
 
 // ---------------------------------------------------------------- tree (tree.cu)
 struct TreeBufs {

@@ -304,6 +304,36 @@ __global__ void __launch_bounds__(256) trunc_fixup_kernel(const uint64_t* __rest
     }
 }
 
+// Small sorts (n <= kSmallSort, e.g. the batch of a small insert): one block ranks each
+// key by counting the (key, index) pairs below it — one launch instead of the
+// histogram, scan and eight one-sweep passes (which cost ~0.1 ms even for one key).
+template <int DIM>
+__global__ void __launch_bounds__(kSmallSort) small_sort_kernel(const int32_t* __restrict__ pts, uint32_t n, uint32_t id_base,
+                                                                int4 psh, uint64_t* __restrict__ keys_out,
+                                                                int4* __restrict__ recs_out, int* __restrict__ invalid) {
+    __shared__ uint64_t s_key[kSmallSort];
+    const uint32_t i = threadIdx.x;
+    bool bad = false;
+    uint64_t k = ~0ull;
+    if (i < n) k = load_key_from_points<DIM>(pts, i, bad, psh);
+    s_key[i] = k;
+    if (__syncthreads_or(bad) && i == 0) atomicOr(invalid, 1);
+    if (i >= n) return;
+    uint32_t rank = 0;   // stable: equal keys keep input (= id) order
+    for (uint32_t j = 0; j < n; ++j) {
+        const uint64_t kj = s_key[j];
+        rank += (kj < k || (kj == k && j < i)) ? 1u : 0u;
+    }
+    keys_out[rank] = k;
+    const uint32_t id = id_base + i;
+    if (DIM == 3 && psh.w == 3) {
+        const int32_t* p = pts + (size_t)i * 3;
+        recs_out[rank] = make_int4(__ldg(p) + psh.x, __ldg(p + 1) + psh.y, __ldg(p + 2) + psh.z, (int)id);
+    } else {
+        recs_out[rank] = decode_rec<DIM>(k, (int)id);
+    }
+}
+
 template <int DIM>
 void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
                    const SortScratch& s, int* d_invalid, int4 psh, cudaStream_t st, int* d_trunc_fail, bool approx) {
@@ -406,6 +436,16 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
 }
 
 }  // namespace
+
+void sort_points_small(int dim, const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* keys_out, int4* recs_out,
+                       int* d_invalid, cudaStream_t st, const int32_t* shift2) {
+    if (n <= 0) return;
+    const int4 psh = shift2 ? make_int4(shift2[0], shift2[1], dim == 3 ? shift2[2] : 0, dim)
+                            : make_int4(0, 0, 0, 0);
+    count_launch(1);
+    if (dim == 2) small_sort_kernel<2><<<1, kSmallSort, 0, st>>>(pts, (uint32_t)n, id_base, psh, keys_out, recs_out, d_invalid);
+    else small_sort_kernel<3><<<1, kSmallSort, 0, st>>>(pts, (uint32_t)n, id_base, psh, keys_out, recs_out, d_invalid);
+}
 
 size_t sort_tiles(int64_t n) { return (size_t)((n + STILE - 1) / STILE); }
 size_t sort_zero_words(int64_t n) { return NPASS * 256 + NPASS + (size_t)NPASS * sort_tiles(n) * 256; }
