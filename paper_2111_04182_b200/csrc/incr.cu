@@ -171,10 +171,10 @@ __global__ void __launch_bounds__(256) incr_refit_kernel(Node<DIM>* __restrict__
 // last dirty child arrives).
 
 // per leaf: dead records (old positions, alive bitset by id), emptied-leaf check,
-// block-exclusive scan into del_before, block totals into bsum.  The grid covers the
-// node capacity; the live leaf count comes from the device meta (meta[0] internal
-// nodes, meta[1] root: a single-leaf tree takes the full rebuild), so the host needs no
-// node count before the launch.
+// block-exclusive scan into del_before, chunk totals into bsum.  The live leaf count
+// comes from the device meta (meta[0] internal nodes, meta[1] root: a single-leaf tree
+// takes the full rebuild), so the host needs no node count before the launch; a fixed
+// grid walks the 256-leaf chunks (no blocks launched for the empty capacity).
 __global__ void __launch_bounds__(256) decr_count_kernel(const int4* __restrict__ recs,
                                                          const int32_t* __restrict__ leaf_start,
                                                          const int32_t* __restrict__ meta,
@@ -182,30 +182,56 @@ __global__ void __launch_bounds__(256) decr_count_kernel(const int4* __restrict_
                                                          uint32_t* __restrict__ bsum, int* __restrict__ bad) {
     __shared__ uint32_t s_warp[32];
     const int32_t nleaves = __ldg(meta) + 1;
-    const int32_t l = blockIdx.x * 256 + threadIdx.x;
-    if (l == 0 && __ldg(meta + 1) < 0) atomicOr(bad, 1);
-    uint32_t c = 0;
-    if (l < nleaves) {
-        const int32_t s = __ldg(leaf_start + l), e = __ldg(leaf_start + l + 1);
-        for (int32_t p = s; p < e; ++p) {
-            const int32_t id = __ldg(recs + p).w;
-            c += ((__ldg(alive + (id >> 5)) >> (id & 31)) & 1u) ? 0u : 1u;
+    const int32_t nchunks = (nleaves + 255) / 256;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && __ldg(meta + 1) < 0) atomicOr(bad, 1);
+    for (int32_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {   // block-uniform
+        const int32_t l = ch * 256 + threadIdx.x;
+        uint32_t c = 0;
+        if (l < nleaves) {
+            const int32_t s = __ldg(leaf_start + l), e = __ldg(leaf_start + l + 1);
+            for (int32_t p = s; p < e; ++p) {
+                const int32_t id = __ldg(recs + p).w;
+                c += ((__ldg(alive + (id >> 5)) >> (id & 31)) & 1u) ? 0u : 1u;
+            }
+            if ((int32_t)c == e - s) atomicOr(bad, 1);   // leaf emptied
         }
-        if ((int32_t)c == e - s) atomicOr(bad, 1);   // leaf emptied
+        uint32_t total;
+        const uint32_t ex = block_exclusive_scan<256>(c, s_warp, &total);
+        if (l < nleaves) del_before[l] = (int32_t)ex;
+        if (threadIdx.x == 0) bsum[ch] = total;
     }
-    uint32_t total;
-    const uint32_t ex = block_exclusive_scan<256>(c, s_warp, &total);
-    if (l < nleaves) del_before[l] = (int32_t)ex;
-    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
 }
 
-// del_before[l] += block offset; del_before[nleaves] = total
+// exclusive scan of the chunk totals (their count from the device meta); bsum[nchunks] = total
+__global__ void __launch_bounds__(1024) decr_scan_kernel(uint32_t* __restrict__ bsum, const int32_t* __restrict__ meta) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_carry;
+    const uint32_t nchunks = (uint32_t)(__ldg(meta) + 1 + 255) / 256;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (uint32_t b0 = 0; b0 < nchunks; b0 += 1024) {
+        const uint32_t i = b0 + threadIdx.x;
+        const uint32_t v = i < nchunks ? bsum[i] : 0u;
+        uint32_t tot;
+        const uint32_t e = block_exclusive_scan<1024>(v, s_warp, &tot);
+        const uint32_t carry = s_carry;
+        if (i < nchunks) bsum[i] = carry + e;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry = carry + tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bsum[nchunks] = s_carry;
+}
+
+// del_before[l] += chunk offset; del_before[nleaves] = total
 __global__ void __launch_bounds__(256) decr_fix_kernel(int32_t* __restrict__ del_before, const int32_t* __restrict__ meta,
-                                                       const uint32_t* __restrict__ bsum, uint32_t nblocks) {
+                                                       const uint32_t* __restrict__ bsum) {
     const int32_t nleaves = __ldg(meta) + 1;
-    const int32_t l = blockIdx.x * 256 + threadIdx.x;
-    if (l < nleaves) del_before[l] += (int32_t)__ldg(bsum + (l >> 8));
-    else if (l == nleaves) del_before[l] = (int32_t)__ldg(bsum + nblocks);
+    const int32_t nchunks = (nleaves + 255) / 256;
+    for (int32_t l = blockIdx.x * 256 + threadIdx.x; l <= nleaves; l += gridDim.x * 256) {
+        if (l < nleaves) del_before[l] += (int32_t)__ldg(bsum + (l >> 8));
+        else del_before[l] = (int32_t)__ldg(bsum + nchunks);
+    }
 }
 
 // every internal node keeps > leaf_max points
@@ -213,12 +239,13 @@ __global__ void __launch_bounds__(256) decr_check_kernel(const int32_t* __restri
                                                          const int32_t* __restrict__ leaf_start,
                                                          const int32_t* __restrict__ del_before, int leaf_max,
                                                          int* __restrict__ bad) {
-    const int32_t i = blockIdx.x * 256 + threadIdx.x;
-    if (i >= __ldg(meta)) return;
-    const int32_t L = __ldg(range + 2 * i), R = __ldg(range + 2 * i + 1);
-    const int32_t size = __ldg(leaf_start + R + 1) - __ldg(leaf_start + L);
-    const int32_t del = __ldg(del_before + R + 1) - __ldg(del_before + L);
-    if (size - del <= leaf_max) atomicOr(bad, 1);
+    const int32_t nb = __ldg(meta);
+    for (int32_t i = blockIdx.x * 256 + threadIdx.x; i < nb; i += gridDim.x * 256) {
+        const int32_t L = __ldg(range + 2 * i), R = __ldg(range + 2 * i + 1);
+        const int32_t size = __ldg(leaf_start + R + 1) - __ldg(leaf_start + L);
+        const int32_t del = __ldg(del_before + R + 1) - __ldg(del_before + L);
+        if (size - del <= leaf_max) atomicOr(bad, 1);
+    }
 }
 
 __global__ void __launch_bounds__(256) decr_leaf_start_kernel(int32_t* __restrict__ leaf_start, int32_t nleaves,
@@ -336,14 +363,18 @@ namespace zd {
 int decr_check(int64_t nb_cap, const int32_t* meta, const int4* recs_old, const int32_t* leaf_start,
                const uint32_t* alive, const int32_t* range, int leaf_max, int32_t* del_before, uint32_t* bsum, int* bad,
                cudaStream_t st) {
+    // fixed grids over the device-side leaf / node counts (the capacity nb_cap may be
+    // ~11x the node count: worst-case sized node buffers below 2^25 points)
     const int64_t nl_cap = nb_cap + 1;
-    const uint32_t nblk = (uint32_t)((nl_cap + 255) / 256);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 8, (nl_cap + 255) / 256));
     count_launch(4);
-    decr_count_kernel<<<nblk, 256, 0, st>>>(recs_old, leaf_start, meta, alive, del_before, bsum, bad);
-    scan_blocks_kernel<<<1, 1024, 0, st>>>(bsum, nblk);
-    decr_fix_kernel<<<(unsigned)((nl_cap + 1 + 255) / 256), 256, 0, st>>>(del_before, meta, bsum, nblk);
-    if (nb_cap > 0)
-        decr_check_kernel<<<(unsigned)((nb_cap + 255) / 256), 256, 0, st>>>(meta, range, leaf_start, del_before, leaf_max, bad);
+    decr_count_kernel<<<g, 256, 0, st>>>(recs_old, leaf_start, meta, alive, del_before, bsum, bad);
+    decr_scan_kernel<<<1, 1024, 0, st>>>(bsum, meta);
+    decr_fix_kernel<<<g, 256, 0, st>>>(del_before, meta, bsum);
+    if (nb_cap > 0) decr_check_kernel<<<g, 256, 0, st>>>(meta, range, leaf_start, del_before, leaf_max, bad);
     return 0;
 }
 
