@@ -421,6 +421,18 @@ def run_gpu(args, D: Dist):
     mean_ph = ph.mean(0)
     knn_ms = float(np.mean(knn_kernel))
 
+    # ---- CPU oracle and per-config report (rank 0 at N=1), measured before the e2e
+    # section: its extra streams and host threads would slow later default-stream
+    # builds (observed +60 us per build), so nothing on the GPU follows it
+    per_q, cpu, per_config = None, None, None
+    if D.rank == 0 and D.world == 1:
+        if args.cpu_baseline:
+            cpu, per_q = cpu_baseline(args.cpu_sample or c["n"])
+        if args.per_config:
+            per_config = run_per_config(zd, dev, clocks)
+    if per_q is None:   # oracle counters of 3D uniform at 10^6 (tests/test_oracle_pins.py App. A pin)
+        per_q = dict(dist_evals=92.0, box_tests=45.0, ascents=9.02, replacements=23.1, evictions=13.1)
+
     # ---- e2e: the same step through the C ABI with pinned HOST buffers
     pts_h = torch.from_numpy(pts_np).pin_memory()
     batch_h = torch.from_numpy(batch_np).pin_memory()
@@ -507,18 +519,6 @@ def run_gpu(args, D: Dist):
 
     if D.rank != 0:
         return
-
-    # ---- CPU oracle on the headline workload (full size by default), rank 0 at N=1
-    per_q, cpu = None, None
-    if args.cpu_baseline and D.world == 1:
-        cpu, per_q = cpu_baseline(args.cpu_sample or c["n"])
-    if per_q is None:   # oracle counters of 3D uniform at 10^6 (tests/test_oracle_pins.py App. A pin)
-        per_q = dict(dist_evals=92.0, box_tests=45.0, ascents=9.02, replacements=23.1, evictions=13.1)
-
-    # ---- per-config report (one GPU): C1-C4b build + k-NN, roofline fractions, parity
-    per_config = None
-    if args.per_config and D.world == 1:
-        per_config = run_per_config(zd, dev, clocks)
 
     # ---- roofline of the dominant kernel (k-NN): issue-bound integer/fp32 ALU work
     sm_max = clocks.get("sm_max_mhz") or 1965.0
