@@ -337,6 +337,40 @@ def load_traffic():
     return None, None
 
 
+def load_work_inflation(per_q):
+    """K6's work against the oracle's (the round-1 verdict's inflation ratios): staged
+    candidates tested per lane and post-seed hits per lane, from the newest committed
+    profiling-build counters `rNN_knn_stats_vMM.jsonl` (scripts/knn_stats.py, config C3,
+    which has the C5 step's point distribution), over the oracle's distance evaluations
+    and k-best insertions per query."""
+    import re
+    pat = re.compile(r"r(\d+)_knn_stats_v(\d+)\.jsonl$")
+    files = []
+    for p in (ROOT / "profiles").glob("r*_knn_stats_v*.jsonl"):
+        m = pat.search(p.name)
+        if m:
+            files.append(((int(m.group(1)), int(m.group(2))), p))
+    for _, p in sorted(files, reverse=True):
+        try:
+            for line in p.read_text().splitlines():
+                if not line.startswith("{"):
+                    continue
+                d = json.loads(line)
+                if d.get("config") != "C3" or d.get("k") != 10:
+                    continue
+                cand = d["per_query"]["candidates_per_lane"]
+                hits = d["per_query"]["hits"]
+                return {"candidates_per_lane": cand, "oracle_dist_evals": per_q["dist_evals"],
+                        "candidates_ratio": cand / per_q["dist_evals"],
+                        "hits_per_lane": hits, "oracle_insertions": per_q["replacements"],
+                        "hits_ratio": hits / per_q["replacements"],
+                        "hit_rounds_per_packet": d["per_packet"]["rounds"],
+                        "source": p.name + " (profiling build, C3) vs the oracle counters of this line"}
+        except Exception:
+            continue
+    return None
+
+
 def run_gpu(args, D: Dist):
     import torch
     import paper_2111_04182_b200 as zd
@@ -524,7 +558,8 @@ def run_gpu(args, D: Dist):
     sm_max = clocks.get("sm_max_mhz") or 1965.0
     knn_roof = knn_roofline(per_q, n_live, knn_ms, sm_max)
     traffic, traffic_src = load_traffic()
-    knn_roof.update({"kernel": "knn_packet_kernel<3,10>", "traffic": traffic, "traffic_source": traffic_src})
+    knn_roof.update({"kernel": "knn_packet_kernel<3,10>", "traffic": traffic, "traffic_source": traffic_src,
+                     "work_inflation": load_work_inflation(per_q)})
     n_before_delete = c["n"] + c["insert_m"]
 
     line = {
