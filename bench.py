@@ -715,7 +715,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-e2e-pipeline", dest="e2e_pipeline", action="store_false",
                     help="e2e steps one after another instead of two overlapping host threads")
     ap.add_argument("--cpu-sample", type=int, default=0, help="C5 points for the oracle baseline (0 = full 10^7)")
