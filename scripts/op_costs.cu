@@ -32,7 +32,7 @@ extern "C" __global__ void op_dist4(const float* __restrict__ in, float wb, int 
     out[threadIdx.x] = hit;
 }
 
-// box test of one child box (knn.cu box_dist + within, 3D fp32)
+// box test of one child box (knn.cu box_dist / gap_d2 + within, 3D fp32)
 extern "C" __global__ void op_box(const float* __restrict__ in, float wb, int iters, uint32_t* out) {
     __shared__ float b[6 * 64];
     for (int t = threadIdx.x; t < 6 * 64; t += blockDim.x) b[t] = in[t];
@@ -43,12 +43,15 @@ extern "C" __global__ void op_box(const float* __restrict__ in, float wb, int it
 #pragma unroll 1
     for (int i = 0; i < iters; ++i) {
         const float* bx = b + 6 * (i & 63);
-        float df = 0.f;
+        // the product's gap_d2: per axis one 3-input max, max(lo - q, q - hi, 0) (FMNMX3)
+        float t[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const float t = fmaxf(bx[a] - qf[a], 0.f) + fmaxf(qf[a] - bx[3 + a], 0.f);
-            df = fmaf(t, t, df);
+            float r;
+            asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(bx[a] - qf[a]), "f"(qf[a] - bx[3 + a]), "f"(0.f));
+            t[a] = r;
         }
+        const float df = fmaf(t[2], t[2], fmaf(t[1], t[1], t[0] * t[0]));
         acc += df <= wb ? 1u : 0u;
     }
     out[threadIdx.x] = acc;
