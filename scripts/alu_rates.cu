@@ -39,6 +39,18 @@ __global__ void k_fmnmx(float* out, float b, float c) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// 3-input fp32 max (FMNMX3 on sm_100a: the k-NN box test's per-axis gap)
+__global__ void k_fmnmx3(float* out, float b, float c) {
+    float a[CH];
+    for (int i = 0; i < CH; ++i) a[i] = threadIdx.x + i;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i) asm volatile("max.f32 %0, %0, %1, %2;" : "+f"(a[i]) : "f"(b), "f"(c));
+    float s = 0;
+    for (int i = 0; i < CH; ++i) s += a[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __global__ void k_iadd3(int* out, int b, int c) {
     int a[CH];
     for (int i = 0; i < CH; ++i) a[i] = threadIdx.x + i;
@@ -125,6 +137,7 @@ int main() {
     int nr = 0;
     res[nr++] = {"FFMA", run([&] { k_ffma<<<blocks, threads>>>((float*)buf, 1.0001f, 0.5f); }, blocks, threads, per)};
     res[nr++] = {"FMNMX", run([&] { k_fmnmx<<<blocks, threads>>>((float*)buf, 1.0f, 2.0f); }, blocks, threads, 2 * per)};
+    res[nr++] = {"FMNMX3", run([&] { k_fmnmx3<<<blocks, threads>>>((float*)buf, 1.0f, 2.0f); }, blocks, threads, per)};
     res[nr++] = {"IMNMX", run([&] { k_imnmx<<<blocks, threads>>>((int*)buf, 3, 1 << 20); }, blocks, threads, 2 * per)};
     res[nr++] = {"IADD", run([&] { k_iadd3<<<blocks, threads>>>((int*)buf, 3, 5); }, blocks, threads, 2 * per)};
     res[nr++] = {"IMAD.WIDE", run([&] { k_imad_wide<<<blocks, threads>>>((long long*)buf, 3, 5); }, blocks, threads, per)};
