@@ -730,6 +730,45 @@ def test_delete_fast_path(zd, oracle_mod, monkeypatch, dist, dim):
     check_rows(gi, gd, oi, od)
 
 
+def test_concurrent_handles_on_streams(zd, oracle_mod):
+    """Different handles used at the same time from two host threads, each on its own
+    CUDA stream with host input and output buffers (bench.py's pipelined e2e): build,
+    insert, delete and the all-points query of each equal the oracle's, and a tree built
+    on a second stream answers like one built on the default stream."""
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+    cases = []
+    for j in range(2):
+        base = zdgen.uniform(20000 + 1000 * j, 3, seed=70 + j)
+        batch = zdgen.uniform(1500, 3, seed=72 + j)
+        kill = zdgen.delete_ids(len(base), 900, seed=74 + j)
+        live = oracle_mod.LiveSet(base)
+        live.insert(batch)
+        live.delete(kill)
+        oi, od, _ = live.tree().knn_all(10)
+        cases.append((base, batch, kill, oi, od))
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    lock = threading.Lock()
+
+    def run(j):
+        base, batch, kill, oi, od = cases[j]
+        with torch.cuda.stream(streams[j]):
+            for _ in range(3):
+                t = zd.zd_build(base, stream=streams[j])      # host input (staged)
+                t.zd_insert(batch)
+                t.zd_delete(kill)
+                gi = np.empty((t.zd_size(), 10), np.int32)
+                gd = np.empty((t.zd_size(), 10), np.int64)
+                t.zd_knn(10, out_idx=gi, out_dist2=gd)          # host output: synchronous
+                t.zd_free()
+                with lock:
+                    check_rows(gi, gd, oi, od)
+        return True
+
+    with ThreadPoolExecutor(2) as ex:
+        assert all(ex.map(run, range(2)))
+
+
 def test_concurrent_knn_one_handle(zd, oracle_mod):
     """zd_knn is re-entrant on one handle ("queries can be conducted in
     parallel"): two host threads query the same tree, after updates (row map) and with
