@@ -21,6 +21,10 @@
 // one record per lane) and broadcast to all lanes; a node whose children are both
 // leaves is scanned as ONE contiguous span (its points are adjacent in sorted order).
 //
+// Scheduling: the first launch is a persistent grid of resident blocks; every warp takes
+// the next packet in Morton order from a counter (packets differ ~2x in cost, so a
+// fixed packet per warp left warps idle until their block's slowest finished).
+//
 // Per-lane k-best state (the warp never serialises on sorted insertions):
 //   fa[K]  ascending list of the k smallest d2 seen so far, each rounded UP to fp32
 //          (ids ignored), kept with branch-free min/max;
