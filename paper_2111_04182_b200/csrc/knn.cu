@@ -425,7 +425,7 @@ __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Qu
 #define ZD_TRANSPOSE_MAX 6   // 2D: at most this many needing lanes: lanes = candidates
 #endif
 #ifndef ZD_TRANSPOSE_MAX3
-#define ZD_TRANSPOSE_MAX3 3  // 3D
+#define ZD_TRANSPOSE_MAX3 1  // 3D (persistent scheduling: 1 beats 2/3/5 and 0)
 #endif
 template <int DIM>
 struct TMax {
