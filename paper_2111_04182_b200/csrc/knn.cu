@@ -419,7 +419,7 @@ __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Qu
 // through shared memory, each lane tests CH of them per uniform pass against its
 // bound, then handles its (few) hits.
 #ifndef ZD_SLACK
-#define ZD_SLACK 4          // uniform compaction when a needing lane has > CAP - SLACK entries
+#define ZD_SLACK 2          // uniform compaction when a needing lane has > CAP - SLACK entries (2: measured best of 0-6)
 #endif
 #ifndef ZD_TRANSPOSE_MAX
 #define ZD_TRANSPOSE_MAX 6   // 2D: at most this many needing lanes: lanes = candidates
