@@ -27,7 +27,7 @@
 //
 // Per-lane k-best state (the warp never serialises on sorted insertions):
 //   fa[K]  ascending list of the k smallest d2 seen so far, each rounded UP to fp32
-//          (ids ignored), kept with branch-free min/max;
+//          (bf16 pairs for even K; ids ignored), kept with branch-free min/max;
 //   U      = ceil(fa[K-1]) as int64: an upper bound on the exact k-th smallest d2 among
 //          the candidates seen, hence on the final k-th distance; U never grows;
 //   buf    (position, ru(d2)) of every candidate that had d2 <= U when seen.
@@ -279,10 +279,60 @@ __device__ __forceinline__ void stf(WarpSh<DIM, K>& S, int j, float4 v) {
 #endif
 constexpr int kSeedW = ZD_SEEDW;
 
+// The ascending list fa of the k smallest candidate upper bounds seen so far (only
+// fa[K-1], the bound, is ever read).  Even K: packed bf16 pairs, every value rounded
+// UP to bf16 (monotone, so fa[K-1] is the bf16 round-up of the fp32 list's last entry:
+// a bound at most 2^-8 looser, never tighter); the median insertion then takes two
+// HMNMX2 and one PRMT per pair instead of four FMNMX, in half the registers.
+#ifndef ZD_FA_BF16
+#define ZD_FA_BF16 1
+#endif
+template <int K, bool PACK = (ZD_FA_BF16 && K % 2 == 0)>
+struct FaList {
+    float v[K];
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int t = 0; t < K; ++t) v[t] = INFINITY;
+    }
+    __device__ __forceinline__ float last() const { return v[K - 1]; }
+    // insert xf, dropping the largest: every new slot is the median of (v[t-1], xf,
+    // v[t]) — all slots independent (depth 2) instead of a K-long compare-exchange
+    // chain; xf >= v[K-1] leaves the list unchanged
+    __device__ __forceinline__ void insert(float xf) {
+#pragma unroll
+        for (int t = K - 1; t > 0; --t) v[t] = fmaxf(v[t - 1], fminf(v[t], xf));
+        v[0] = fminf(v[0], xf);
+    }
+};
+template <int K>
+struct FaList<K, true> {
+    uint32_t p[K / 2];   // pair t = (v[2t] in the low half, v[2t+1] in the high half)
+    __device__ __forceinline__ void init() {
+#pragma unroll
+        for (int t = 0; t < K / 2; ++t) p[t] = 0x7f807f80u;   // (+inf, +inf)
+    }
+    __device__ __forceinline__ float last() const { return __uint_as_float(p[K / 2 - 1] & 0xffff0000u); }
+    __device__ __forceinline__ void insert(float xf) {
+        // bf16 round-up of xf >= 0 (+inf stays +inf) in both halves
+        uint32_t x;
+        asm("prmt.b32 %0, %1, 0, 0x3232;" : "=r"(x) : "r"(__float_as_uint(xf) + 0xffffu));
+        uint32_t sh[K / 2];   // (v[2t-1], v[2t]) from the old pairs; v[-1] = +0
+        sh[0] = p[0] << 16;
+#pragma unroll
+        for (int t = 1; t < K / 2; ++t) asm("prmt.b32 %0, %1, %2, 0x5432;" : "=r"(sh[t]) : "r"(p[t - 1]), "r"(p[t]));
+#pragma unroll
+        for (int t = 0; t < K / 2; ++t) {
+            uint32_t m;
+            asm("min.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(p[t]), "r"(x));
+            asm("max.bf16x2 %0, %1, %2;" : "=r"(p[t]) : "r"(sh[t]), "r"(m));
+        }
+    }
+};
+
 template <int DIM, int K>
 struct Lane {
     Query<DIM> q;
-    float fa[K];
+    FaList<K> fa;
     int64_t U;          // -1 for an idle lane: needs nothing, accepts nothing
     float qf[3];        // 3D fp32 filter: the query in fp32 (exact)
     float wb;           //   and a bound with d2 <= U  =>  fp32 d2 <= wb
@@ -295,7 +345,7 @@ struct Lane {
 
 template <int DIM, int K>
 __device__ __forceinline__ void set_bound(Lane<DIM, K>& L) {
-    const float f = L.fa[K - 1];
+    const float f = L.fa.last();
     if (DIM == 3) {
         // 3D: coordinates and their differences are exact in fp32 and the three rounded
         // products/sums make the fp32 d2 at most (1 + 3.0000002 * 2^-24) times the
@@ -362,7 +412,7 @@ __device__ __forceinline__ bool lane_stop(const Lane<DIM, K>& L, const typename 
         for (int a = 0; a < 3; ++a) m = fminf(m, fminf(L.qf[a] - b[a], b[3 + a] - L.qf[a]));
         if (m < 0.f) return false;
         const float mm = m + 1.0f;
-        return __fmul_rd(mm, mm) > L.fa[K - 1];
+        return __fmul_rd(mm, mm) > L.fa.last();
     } else {
         return stop_at<DIM>(L.q, b, L.U);
     }
@@ -374,7 +424,7 @@ template <int DIM, int K>
 __device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<DIM, K>& S, int lane) {
     // 3D buffers fp32-derived upper bounds ub with d2 <= ub <= d2 (1 + 2^-20): a final
     // neighbour has ub <= D_k (1 + 2^-20) <= fa[K-1] (1 + 2^-20)
-    const float F = DIM == 3 ? __fmul_ru(L.fa[K - 1], 1.0f + 0x1p-20f) : L.fa[K - 1];
+    const float F = DIM == 3 ? __fmul_ru(L.fa.last(), 1.0f + 0x1p-20f) : L.fa.last();
     int w = 0;
     for (int e = 0; e < L.cnt; ++e) {
         const int2 v = S.be[e][lane];
@@ -385,15 +435,6 @@ __device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<DIM, K>& S, int 
     L.cnt = w;
 }
 
-// Insert xf into the sorted list fa, dropping the largest: every new slot is the
-// median of (fa[t-1], xf, fa[t]) — all slots independent (depth 2) instead of a
-// K-long compare-exchange chain.  xf >= fa[K-1] leaves fa unchanged.
-template <int K>
-__device__ __forceinline__ void fa_insert(float (&fa)[K], float xf) {
-#pragma unroll
-    for (int t = K - 1; t > 0; --t) fa[t] = fmaxf(fa[t - 1], fminf(fa[t], xf));
-    fa[0] = fminf(fa[0], xf);
-}
 
 // Rare path (massive distance ties survive compaction): keep only the exact K best
 // buffered candidates by (d2, id).  Entries ranked >= K are marked +inf and dropped
@@ -685,7 +726,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 if (L.seed) atomicAdd(&g_knn_stats[ZS_SEED_INS], 1ull);
                 if (L.cnt == Cap<DIM, K>::v) atomicAdd(&g_knn_stats[ZS_LANE_COMPACT], 1ull);
 #endif
-                fa_insert<K>(L.fa, xf);
+                L.fa.insert(xf);
                 set_bound<DIM, K>(L);
                 if (L.cnt == Cap<DIM, K>::v) {   // rare: per-lane compaction
                     compact<DIM, K>(L, S, lane);
@@ -744,7 +785,7 @@ __device__ __forceinline__ void seed_scan(const int4* __restrict__ recs, int32_t
                         cid = c.w;
                     }
                     if (!active || cid == L.q.id) xf = INFINITY;
-                    if (__any_sync(0xffffffffu, xf < L.fa[K - 1])) fa_insert<K>(L.fa, xf);
+                    if (__any_sync(0xffffffffu, xf < L.fa.last())) L.fa.insert(xf);
                 }
             } else {
                 const float wb = L.wb;
@@ -840,7 +881,7 @@ __device__ __forceinline__ void window_seed(const int4* __restrict__ recs, int32
             const bool valid = active && c.w >= 0;
             if (pass == 0) {
                 if (!valid) xf = INFINITY;
-                if (__any_sync(0xffffffffu, xf < L.fa[K - 1])) fa_insert<K>(L.fa, xf);
+                if (__any_sync(0xffffffffu, xf < L.fa.last())) L.fa.insert(xf);
             } else if (valid && in) {
                 if (L.cnt == Cap<DIM, K>::v) {   // rare (ties): keep the exact K best
                     compact<DIM, K>(L, S, lane);
@@ -1019,8 +1060,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
     Lane<DIM, K> L;
     L.q.c[0] = r.x; L.q.c[1] = r.y; L.q.c[2] = r.z;
     L.q.id = EXT ? -1 : r.w;
-#pragma unroll
-    for (int t = 0; t < K; ++t) L.fa[t] = INFINITY;
+    L.fa.init();
     L.U = active ? INT64_MAX : (int64_t)-1;   // an idle lane needs nothing, accepts nothing
     L.qf[0] = __int2float_rn(r.x); L.qf[1] = __int2float_rn(r.y); L.qf[2] = __int2float_rn(r.z);
     L.wb = active ? INFINITY : -1.0f;
@@ -1128,12 +1168,12 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
             const float e = (float)(mx - mn);
             ext2 = fmaxf(ext2, e * e);
         }
-        const bool fin = active && L.fa[K - 1] != INFINITY;
+        const bool fin = active && L.fa.last() != INFINITY;
         const int nfin = __popc(__ballot_sync(0xffffffffu, fin));
         const int nact = __popc(__ballot_sync(0xffffffffu, active));
         // median over the active lanes of log2(bound + 1) (bitonic sort across the warp;
         // idle lanes sort last)
-        float v = active ? (fin ? __log2f(L.fa[K - 1] + 1.0f) : 1e30f) : INFINITY;
+        float v = active ? (fin ? __log2f(L.fa.last() + 1.0f) : 1e30f) : INFINITY;
 #pragma unroll
         for (int kk = 2; kk <= 32; kk <<= 1) {
 #pragma unroll

@@ -104,6 +104,45 @@ __global__ void k_cmp64(long long* out, long long b, long long c) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// packed bf16x2 / f16x2 min + max (HMNMX2): candidate k-best list in packed halves
+__global__ void k_hmnmx2_bf16(unsigned* out, unsigned b, unsigned c) {
+    unsigned a[CH];
+    for (int i = 0; i < CH; ++i) a[i] = 0x3f803f80u + threadIdx.x + i;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            asm volatile("max.bf16x2 %0, %0, %1;" : "+r"(a[i]) : "r"(b));
+            asm volatile("min.bf16x2 %0, %0, %1;" : "+r"(a[i]) : "r"(c));
+        }
+    unsigned s = 0;
+    for (int i = 0; i < CH; ++i) s += a[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_hmnmx2_f16(unsigned* out, unsigned b, unsigned c) {
+    unsigned a[CH];
+    for (int i = 0; i < CH; ++i) a[i] = 0x3c003c00u + threadIdx.x + i;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            asm volatile("max.f16x2 %0, %0, %1;" : "+r"(a[i]) : "r"(b));
+            asm volatile("min.f16x2 %0, %0, %1;" : "+r"(a[i]) : "r"(c));
+        }
+    unsigned s = 0;
+    for (int i = 0; i < CH; ++i) s += a[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// byte permute (PRMT): pairs the halves of two packed registers
+__global__ void k_prmt(unsigned* out, unsigned b, unsigned c) {
+    unsigned a[CH];
+    for (int i = 0; i < CH; ++i) a[i] = threadIdx.x + i;
+    for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+        for (int i = 0; i < CH; ++i) asm volatile("prmt.b32 %0, %0, %1, 0x5432;" : "+r"(a[i]) : "r"(b));
+    unsigned s = 0;
+    for (int i = 0; i < CH; ++i) s += a[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename F>
 static double run(F launch, int blocks, int threads, double ops_per_thread) {
     cudaEvent_t e0, e1;
@@ -133,7 +172,7 @@ int main() {
     void* buf = nullptr;
     cudaMalloc(&buf, (size_t)blocks * threads * 8);
     const double per = (double)ITERS * CH;
-    struct R { const char* name; double ops; } res[8];
+    struct R { const char* name; double ops; } res[12];
     int nr = 0;
     res[nr++] = {"FFMA", run([&] { k_ffma<<<blocks, threads>>>((float*)buf, 1.0001f, 0.5f); }, blocks, threads, per)};
     res[nr++] = {"FMNMX", run([&] { k_fmnmx<<<blocks, threads>>>((float*)buf, 1.0f, 2.0f); }, blocks, threads, 2 * per)};
@@ -142,6 +181,9 @@ int main() {
     res[nr++] = {"IADD", run([&] { k_iadd3<<<blocks, threads>>>((int*)buf, 3, 5); }, blocks, threads, 2 * per)};
     res[nr++] = {"IMAD.WIDE", run([&] { k_imad_wide<<<blocks, threads>>>((long long*)buf, 3, 5); }, blocks, threads, per)};
     res[nr++] = {"ISETP64+SEL", run([&] { k_cmp64<<<blocks, threads>>>((long long*)buf, 1000, 7); }, blocks, threads, per)};
+    res[nr++] = {"HMNMX2.BF16 (pairs)", run([&] { k_hmnmx2_bf16<<<blocks, threads>>>((unsigned*)buf, 0x3f003f00u, 0x40004000u); }, blocks, threads, 2 * per)};
+    res[nr++] = {"HMNMX2.F16 (pairs)", run([&] { k_hmnmx2_f16<<<blocks, threads>>>((unsigned*)buf, 0x38003800u, 0x40004000u); }, blocks, threads, 2 * per)};
+    res[nr++] = {"PRMT", run([&] { k_prmt<<<blocks, threads>>>((unsigned*)buf, 7u, 0u); }, blocks, threads, per)};
     printf("{\"sms\": %d, \"clock_attr_mhz\": %.0f, \"ops\": {", sms, clk_khz / 1e3);
     for (int i = 0; i < nr; ++i)
         printf("%s\"%s\": {\"lane_ops_per_s\": %.4g}", i ? ", " : "", res[i].name, res[i].ops);
