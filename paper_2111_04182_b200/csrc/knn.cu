@@ -166,7 +166,7 @@ struct Pw {
 #ifndef ZD_CH
 #define ZD_CH 32
 #endif
-constexpr int CH = ZD_CH;                // candidates tested per uniform pass
+[[maybe_unused]] constexpr int CH = ZD_CH;                // candidates tested per uniform pass
 constexpr int32_t kNoSub = INT32_MIN;    // no subtree pending
 #ifndef ZD_STK
 #define ZD_STK kMaxDepth
@@ -237,6 +237,9 @@ constexpr int kPG = ZD_PREGROUPS, kPGW = 32 / ZD_PREGROUPS;
 #endif
 #ifndef ZD_SUB3
 #define ZD_SUB3 4        // 3D
+#endif
+#ifndef ZD_SIGNMASK
+#define ZD_SIGNMASK 1    // uniform tests: hit mask from the sign bits of wb - s (3D), U - d2 (2D)
 #endif
 #ifndef ZD_COOP_OUT
 #define ZD_COOP_OUT 1    // stage the packet's output rows in shared memory, write them coalesced
@@ -369,6 +372,13 @@ __device__ __forceinline__ float gap_d2(const float (&q)[3], const float* b) {
     const float ty = fmax3(b[1] - q[1], q[1] - b[4], 0.f);
     const float tz = fmax3(b[2] - q[2], q[2] - b[5], 0.f);
     return fmaf(tz, tz, fmaf(ty, ty, tx * tx));
+}
+
+// (m << 1) | sign bit of x: one funnel shift
+__device__ __forceinline__ uint32_t shl_sign(uint32_t m, float x) {
+    uint32_t r;
+    asm("shf.l.wrap.b32 %0, %1, %2, 1;" : "=r"(r) : "r"(__float_as_uint(x)), "r"(m));
+    return r;
 }
 
 // Box distance in the lane's test domain: fp32 (3D) or exact int64 (2D).
@@ -584,6 +594,32 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                     const float wb = L.wb;
                     const float2 qx = make_float2(L.qf[0], L.qf[0]), qy = make_float2(L.qf[1], L.qf[1]),
                                  qz = make_float2(L.qf[2], L.qf[2]);
+#if ZD_SIGNMASK
+                    // a miss is a negative wb - s (the exact sign of an fp32 difference: the
+                    // same decision as s <= wb); each sign bit is shifted into the mask by
+                    // one funnel shift, the mask is bit-reversed once per pass
+                    const float2 wb2 = make_float2(wb, wb);
+                    uint32_t miss = 0;
+                    int j0 = 0;
+#pragma unroll 1
+                    for (; j0 < cnt; j0 += 4) {
+                        const float4 X = *reinterpret_cast<const float4*>(&S.fx[h0 + j0]);
+                        const float4 Y = *reinterpret_cast<const float4*>(&S.fy[h0 + j0]);
+                        const float4 Z = *reinterpret_cast<const float4*>(&S.fz[h0 + j0]);
+                        const float2 dx0 = __fadd2_rn(qx, make_float2(-X.x, -X.y)), dx1 = __fadd2_rn(qx, make_float2(-X.z, -X.w));
+                        const float2 dy0 = __fadd2_rn(qy, make_float2(-Y.x, -Y.y)), dy1 = __fadd2_rn(qy, make_float2(-Y.z, -Y.w));
+                        const float2 dz0 = __fadd2_rn(qz, make_float2(-Z.x, -Z.y)), dz1 = __fadd2_rn(qz, make_float2(-Z.z, -Z.w));
+                        const float2 s0 = __ffma2_rn(dz0, dz0, __ffma2_rn(dy0, dy0, __fmul2_rn(dx0, dx0)));
+                        const float2 s1 = __ffma2_rn(dz1, dz1, __ffma2_rn(dy1, dy1, __fmul2_rn(dx1, dx1)));
+                        const float2 m0 = __fadd2_rn(wb2, make_float2(-s0.x, -s0.y));
+                        const float2 m1 = __fadd2_rn(wb2, make_float2(-s1.x, -s1.y));
+                        miss = shl_sign(miss, m0.x);
+                        miss = shl_sign(miss, m0.y);
+                        miss = shl_sign(miss, m1.x);
+                        miss = shl_sign(miss, m1.y);
+                    }
+                    hit = ~(__brev(miss) >> (32 - j0));   // j0 = 4 ceil(cnt / 4) >= 4; candidate j at bit j
+#else
 #pragma unroll 1
                     for (int j0 = 0; j0 < CH; j0 += ZD_SUB3) {
                         if (j0 >= cnt) break;
@@ -602,8 +638,25 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                             hit |= hb << j1;
                         }
                     }
+#endif
                 } else {
                     const int64_t U = L.U;
+#if ZD_SIGNMASK
+                    // miss iff U - d2 < 0 (no overflow: 0 <= d2 < 2^63, -1 <= U), the sign
+                    // bits funnel-shifted into the mask as in 3D
+                    uint32_t miss = 0;
+                    int j0 = 0;
+#pragma unroll 1
+                    for (; j0 < cnt; j0 += ZD_SUB) {
+#pragma unroll
+                        for (int jj = 0; jj < ZD_SUB; ++jj) {
+                            const int4 c = S.c[h0 + j0 + jj];
+                            const int64_t m = U - dist2<DIM>(L.q, c);
+                            miss = shl_sign(miss, __int_as_float((int)(m >> 32)));
+                        }
+                    }
+                    hit = ~(__brev(miss) >> (32 - j0));   // j0 = ZD_SUB ceil(cnt / ZD_SUB)
+#else
 #pragma unroll 1
                     for (int j0 = 0; j0 < CH; j0 += ZD_SUB) {
                         if (j0 >= cnt) break;
@@ -614,6 +667,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                             if (dist2<DIM>(L.q, c) <= U) hit |= 1u << j;
                         }
                     }
+#endif
                 }
                 hit &= cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
 #else
