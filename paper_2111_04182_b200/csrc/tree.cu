@@ -303,12 +303,19 @@ __device__ __forceinline__ void store_box(typename BoxT<DIM>::T* dst, const int3
 }
 
 // One block per window of BW consecutive leaves.  An internal node whose whole leaf
-// range lies in the window gets both of its arrivals from this block, so its arrival
-// counter lives in shared memory and the release/acquire pair is block-scoped (no
-// device fence, no L1 invalidation); only window-crossing nodes use the device-scope
-// protocol.  A node's range is bounded by the nearest larger split bit on each side
-// (the canonical tree is the Cartesian tree of the split bits), found by scanning the
-// window's split bits in shared memory.
+// range lies in the window ("local") gets both of its arrivals from this block: a node's
+// range is bounded by the nearest larger split bit on each side (the canonical tree is
+// the Cartesian tree of the split bits), found by prefix / suffix max scans of the
+// window's split bits.
+//   1. leaf boxes, then the climb through local nodes: children's boxes, leaf bounds,
+//      refs and parent links go through shared memory only (block-scoped
+//      release/acquire on a shared arrival counter; no global store or device fence
+//      inside the dependent chain);
+//   2. after a block barrier, thread t writes the complete record of local node b0+t
+//      (one contiguous 48/64-byte store per thread), its leaf bounds and point range,
+//      and leaf b0+t's parent;
+//   3. the threads that reached a window-crossing parent continue with device-scope
+//      acq_rel arrival counters in global memory (a crossing node's ancestors all cross).
 #ifndef ZD_BU_WINDOW
 #define ZD_BU_WINDOW 128
 #endif
@@ -320,15 +327,18 @@ constexpr int kLeafUnroll = ZD_LEAF_UNROLL;   // leaf-box record loads in flight
 
 template <int DIM>
 __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ recs, const int32_t* __restrict__ leaf_start,
-                                                       const int32_t* __restrict__ split_bit, int32_t* meta,
-                                                       Node<DIM>* nodes, int32_t* __restrict__ leaf_parent,
-                                                       uint32_t* visit, int32_t* range, int2* __restrict__ pos_range) {
+                                                        const int32_t* __restrict__ split_bit, int32_t* meta,
+                                                        Node<DIM>* nodes, int32_t* __restrict__ leaf_parent,
+                                                        uint32_t* visit, int32_t* range, int2* __restrict__ pos_range) {
+    using BT = typename BoxT<DIM>::T;
     __shared__ int32_t s_sb[BW + 1];      // split bits of nodes b0-1 .. b0+BW-1 (INT32_MAX outside [0, nb))
     __shared__ int32_t s_ls[BW + 1];      // leaf_start[b0 .. b0+BW]
     __shared__ uint8_t s_local[BW];       // node b0+t finishes inside this block
     __shared__ uint32_t s_visit[BW];      // block-local arrival counters
-    __shared__ int32_t s_rng[BW][2];      // block-local nodes: children's leaf bounds (L of left, R of right)
-    __shared__ __align__(8) int32_t s_box[BW][2][2 * DIM];   // block-local nodes: children's boxes
+    __shared__ int32_t s_rng[BW][2];      // local nodes: children's leaf bounds (L of left, R of right)
+    __shared__ int32_t s_cref[BW][2];     // local nodes: child refs
+    __shared__ int32_t s_par[BW];         // local nodes: parent (-1 until a child of the parent sets it)
+    __shared__ __align__(8) int32_t s_box[BW][2][2 * DIM];   // local nodes: children's boxes
     const int32_t nb = meta[0];
     const int32_t b0 = blockIdx.x * BW;
     if (b0 > nb) return;                  // block-uniform
@@ -340,8 +350,6 @@ __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ 
     }
     __syncthreads();
     {
-        // node b0+t (= s_sb[t+1]) is window-local iff a larger split bit exists in
-        // s_sb[0..t] and in s_sb[t+2..BW]: a block prefix-max and suffix-max scan
         __shared__ int32_t s_wmax[2][BW / 32];
         __shared__ int32_t s_suf[BW];
         const int lane = t & 31, wi = t >> 5;
@@ -368,19 +376,33 @@ __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ 
         }
         s_local[t] = loc;
         s_visit[t] = 0u;
+        s_par[t] = -1;
     }
     __syncthreads();
     const int32_t l = b0 + t;
-    if (l > nb) return;
-    // split bit of node q / start of leaf q, from shared memory inside the window
+    if (nb == 0) {                        // block-uniform: a single leaf (only block 0 gets here)
+        if (t == 0) leaf_parent[0] = -1;
+        return;
+    }
     auto sbit = [&](int32_t q) { return (q >= b0 - 1 && q < b0 + BW) ? s_sb[q - b0 + 1] : __ldg(split_bit + q); };
     auto lstart = [&](int32_t q) { return (q >= b0 && q <= b0 + BW) ? s_ls[q - b0] : __ldg(leaf_start + q); };
-    {
-        // leaf box from its records (independent loads, unrolled)
-        int32_t bb[2 * DIM];
+    // parent of the subtree spanning leaves [L, R]: the boundary node with the smaller split bit
+    auto parent_of = [&](int32_t L, int32_t R, bool& as_right) {
+        if (L == 0) { as_right = false; return R; }
+        if (R == nb) { as_right = true; return L - 1; }
+        if (sbit(L - 1) < sbit(R)) { as_right = true; return L - 1; }
+        as_right = false;
+        return R;
+    };
+    int32_t bb[2 * DIM];
+    int32_t L = l, R = l, ref = -1, s = 0, e = 0, lp = -1;
+    bool pending = false;
 #pragma unroll
-        for (int a = 0; a < DIM; ++a) { bb[a] = INT32_MAX; bb[DIM + a] = INT32_MIN; }
-        const int32_t s = s_ls[t], e = lstart(l + 1);
+    for (int a = 0; a < DIM; ++a) { bb[a] = INT32_MAX; bb[DIM + a] = INT32_MIN; }
+    if (l <= nb) {
+        s = s_ls[t];
+        e = lstart(l + 1);
+        // leaf box from its records (independent loads, unrolled)
 #pragma unroll kLeafUnroll
         for (int32_t j = s; j < e; ++j) {
             const int4 r = __ldg(recs + j);
@@ -388,66 +410,87 @@ __global__ void __launch_bounds__(BW) bottom_up_kernel(const int4* __restrict__ 
 #pragma unroll
             for (int a = 0; a < DIM; ++a) { bb[a] = min(bb[a], c[a]); bb[DIM + a] = max(bb[DIM + a], c[a]); }
         }
-        if (nb == 0) { leaf_parent[0] = -1; return; }
-        int32_t L = l, R = l, ref = -1;   // ref: internal node index, -1 while at the leaf
+        // window-relative climb: the subtree's leaves stay inside the window, so both
+        // boundary split bits are in s_sb (the INT32_MAX sentinels outside [0, nb) make
+        // L == 0 choose R and R == nb choose L - 1, as parent_of does)
+        int Lr = t, Rr = t;
         while (true) {
-            bool as_right;
-            int32_t par;
-            if (L == 0) { par = R; as_right = false; }
-            else if (R == nb) { par = L - 1; as_right = true; }
-            else if (sbit(L - 1) < sbit(R)) { par = L - 1; as_right = true; }
-            else { par = R; as_right = false; }
-            ZD_DCHECK(par >= 0 && par < nb && L >= 0 && R <= nb);
-            Node<DIM>* P = nodes + par;
+            const bool as_right = s_sb[Lr] < s_sb[Rr + 1];
+            const int pi = as_right ? Lr - 1 : Rr;
+            if (pi < 0 || pi >= BW || !s_local[pi]) { pending = true; break; }
+            const int side = as_right ? 1 : 0;
+            const int32_t par = b0 + pi;
+#pragma unroll
+            for (int a = 0; a < DIM; ++a)
+                reinterpret_cast<int2*>(s_box[pi][side])[a] = make_int2(bb[2 * a], bb[2 * a + 1]);
+            s_rng[pi][side] = b0 + (as_right ? Rr : Lr);
             // a leaf child is encoded by its point range: left = ~start, right = ~end
-            const int32_t cref = ref >= 0 ? ref : (as_right ? ~e : ~s);
-            const bool loc = par >= b0 && par < b0 + BW && s_local[par - b0];
-            if (as_right) { store_box<DIM>(P->rbox, bb); P->right = cref; }
-            else { store_box<DIM>(P->lbox, bb); P->left = cref; }
-            range[2 * par + (as_right ? 1 : 0)] = as_right ? R : L;   // leaf bounds (also read by the delete check)
-            if (ref < 0) leaf_parent[l] = par; else nodes[ref].parent = par;
-            if (loc) {
-                // both children of par finish in this block: exchange through shared
-                // memory with a block-scoped release/acquire
-                const int pi = par - b0, side = as_right ? 1 : 0;
+            s_cref[pi][side] = ref >= 0 ? ref : (as_right ? ~e : ~s);
+            if (ref < 0) lp = par; else s_par[ref - b0] = par;   // a local node's children are local
+            __threadfence_block();
+            if (atomicAdd(&s_visit[pi], 1u) == 0) break;          // first child: the sibling finishes the parent
+            __threadfence_block();
 #pragma unroll
-                for (int a = 0; a < DIM; ++a)
-                    reinterpret_cast<int2*>(s_box[pi][side])[a] = make_int2(bb[2 * a], bb[2 * a + 1]);
-                s_rng[pi][side] = as_right ? R : L;
-                __threadfence_block();
-                if (atomicAdd(&s_visit[pi], 1u) == 0) break;
-                __threadfence_block();
-                int32_t ob[2 * DIM];
-#pragma unroll
-                for (int a = 0; a < DIM; ++a) {
-                    const int2 v = reinterpret_cast<const int2*>(s_box[pi][side ^ 1])[a];
-                    ob[2 * a] = v.x;
-                    ob[2 * a + 1] = v.y;
-                }
-#pragma unroll
-                for (int a = 0; a < DIM; ++a) {
-                    bb[a] = min(bb[a], ob[a]);
-                    bb[DIM + a] = max(bb[DIM + a], ob[DIM + a]);
-                }
-                if (as_right) L = s_rng[pi][0]; else R = s_rng[pi][1];
-            } else {
-                // release: our writes are visible before the count; acquire: the second
-                // arriver sees its sibling's
-                const uint32_t arrived =
-                    cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(visit[par]).fetch_add(1u, cuda::memory_order_acq_rel);
-                if (arrived == 0) break;   // first child: the sibling finishes the parent
-                const typename BoxT<DIM>::T* sb = as_right ? P->lbox : P->rbox;
-#pragma unroll
-                for (int a = 0; a < DIM; ++a) {
-                    bb[a] = min(bb[a], (int32_t)__ldcg(sb + a));
-                    bb[DIM + a] = max(bb[DIM + a], (int32_t)__ldcg(sb + DIM + a));
-                }
-                if (as_right) L = __ldcg(range + 2 * par); else R = __ldcg(range + 2 * par + 1);
+            for (int a = 0; a < DIM; ++a) {
+                const int2 v = reinterpret_cast<const int2*>(s_box[pi][side ^ 1])[a];
+                const int32_t o0 = v.x, o1 = v.y;   // entries 2a, 2a+1 of the sibling's box
+                if (2 * a < DIM) bb[2 * a] = min(bb[2 * a], o0); else bb[2 * a] = max(bb[2 * a], o0);
+                if (2 * a + 1 < DIM) bb[2 * a + 1] = min(bb[2 * a + 1], o1); else bb[2 * a + 1] = max(bb[2 * a + 1], o1);
             }
-            pos_range[par] = make_int2(lstart(L), lstart(R + 1));
+            if (as_right) Lr = s_rng[pi][0] - b0; else Rr = s_rng[pi][1] - b0;
             ref = par;
-            if (L == 0 && R == nb) { P->parent = -1; meta[1] = par; break; }
+            if (b0 + Lr == 0 && b0 + Rr == nb) { meta[1] = par; break; }      // the root is local: its parent stays -1
         }
+        L = b0 + Lr;
+        R = b0 + Rr;
+    }
+    __syncthreads();
+    if (lp >= 0) leaf_parent[l] = lp;
+    if (l < nb && s_local[t]) {
+        Node<DIM> nd;
+#pragma unroll
+        for (int a = 0; a < 2 * DIM; ++a) {
+            nd.lbox[a] = (BT)s_box[t][0][a];   // exact (3D: < 2^21)
+            nd.rbox[a] = (BT)s_box[t][1][a];
+        }
+        nd.left = s_cref[t][0];
+        nd.right = s_cref[t][1];
+        nd.parent = s_par[t];
+        nd.mid = s_ls[t + 1];
+        int4* dst = reinterpret_cast<int4*>(nodes + l);
+        const int4* src = reinterpret_cast<const int4*>(&nd);
+#pragma unroll
+        for (int i = 0; i < (int)(sizeof(Node<DIM>) / 16); ++i) dst[i] = src[i];
+        const int32_t nl = s_rng[t][0], nr = s_rng[t][1];
+        *reinterpret_cast<int2*>(range + 2 * l) = make_int2(nl, nr);
+        pos_range[l] = make_int2(s_ls[nl - b0], s_ls[nr + 1 - b0]);
+    }
+    __syncthreads();   // the records written above precede the parent links written below
+    if (!pending) return;
+    while (true) {
+        bool as_right;
+        const int32_t par = parent_of(L, R, as_right);
+        ZD_DCHECK(par >= 0 && par < nb && L >= 0 && R <= nb);
+        Node<DIM>* P = nodes + par;
+        const int32_t cref = ref >= 0 ? ref : (as_right ? ~e : ~s);
+        if (as_right) { store_box<DIM>(P->rbox, bb); P->right = cref; }
+        else { store_box<DIM>(P->lbox, bb); P->left = cref; }
+        range[2 * par + (as_right ? 1 : 0)] = as_right ? R : L;   // leaf bounds (also read by the delete check)
+        if (ref < 0) leaf_parent[l] = par; else nodes[ref].parent = par;
+        // release: our writes are visible before the count; acquire: the second arriver sees its sibling's
+        const uint32_t arrived =
+            cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(visit[par]).fetch_add(1u, cuda::memory_order_acq_rel);
+        if (arrived == 0) break;   // first child: the sibling finishes the parent
+        const BT* sb = as_right ? P->lbox : P->rbox;
+#pragma unroll
+        for (int a = 0; a < DIM; ++a) {
+            bb[a] = min(bb[a], (int32_t)__ldcg(sb + a));
+            bb[DIM + a] = max(bb[DIM + a], (int32_t)__ldcg(sb + DIM + a));
+        }
+        if (as_right) L = __ldcg(range + 2 * par); else R = __ldcg(range + 2 * par + 1);
+        pos_range[par] = make_int2(lstart(L), lstart(R + 1));
+        ref = par;
+        if (L == 0 && R == nb) { P->parent = -1; meta[1] = par; break; }
     }
 }
 

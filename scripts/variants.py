@@ -9,7 +9,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-VARIANTS = json.loads(os.environ.get("ZD_VARIANTS", "{}")) or {
+_VJ = ROOT / "build_var" / "variants.json"   # written by build, read by run (the GPU box has no env)
+VARIANTS = json.loads(os.environ.get("ZD_VARIANTS") or (_VJ.read_text() if _VJ.exists() and len(sys.argv) > 1 and sys.argv[1] == "run" else "{}")) or {
     "A_default": [],
     "B_uniform": ["ZD_OWNER_MAX=0"],
     "C_owner8": ["ZD_OWNER_MAX=8"],
@@ -25,6 +26,7 @@ def build():
     out.mkdir(exist_ok=True)
     for old in out.glob("*.so"):   # only the current variants travel to the GPU box
         old.unlink()
+    _VJ.write_text(json.dumps(VARIANTS))
     with ThreadPoolExecutor(4) as ex:
         list(ex.map(lambda kv: zd.build_lib(force=True, defines=kv[1], out=out / f"{kv[0]}.so"), VARIANTS.items()))
 
