@@ -43,6 +43,28 @@ def test_sort_and_structure_sizes(zd, oracle_mod, n, dim):
     assert t.zd_size() == n
 
 
+@pytest.mark.parametrize("n", [127, 128, 129, 130, 255, 256, 257, 383, 384, 385, 1153])
+@pytest.mark.parametrize("dim", [2, 3])
+def test_bottom_up_window_boundaries(zd, oracle_mod, n, dim):
+    """leaf_max = 1 makes every point a leaf, so the leaf count sits on and around the
+    bottom-up pass's 128-leaf windows: window-local nodes (written from shared memory
+    after the block barrier) and window-crossing nodes (device-scope arrivals) must
+    give the oracle's tree; the k-NN reads the nodes' point ranges, the delete fast
+    path their leaf bounds."""
+    pts = zdgen.uniform(n, dim, seed=900 + n)
+    t = zd.zd_build(dev(pts), leaf_max=1)
+    ot = oracle_mod.Tree(pts, leaf_max=1)
+    assert_same_structure(t.zd_export(), ot)
+    gi, gd = gpu_knn_all(t, 3)
+    oi, od, _ = ot.knn_all(3)
+    check_rows(gi, gd, oi, od)
+    kill = np.array([n // 2], np.int32)
+    assert t.zd_delete(dev(kill)) == 1
+    live = oracle_mod.LiveSet(pts, leaf_max=1)
+    live.delete(kill)
+    assert_same_structure(t.zd_export(), live.tree())
+
+
 @pytest.mark.parametrize("dist,dim", [("uniform", 2), ("uniform", 3), ("plummer", 3), ("sphere", 3),
                                       ("dup", 2), ("dup", 3)])
 @pytest.mark.parametrize("leaf_max", [1, 4, 16, 32])
