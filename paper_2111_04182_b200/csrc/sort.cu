@@ -66,34 +66,36 @@ __device__ __forceinline__ uint64_t load_key_from_points(const int32_t* __restri
     return shifted_key<DIM>(x, y, z, sh);
 }
 
-// Up-front histogram of all 8 digits (+ range validation).
-template <int DIM>
+// Up-front histogram of the digits P0..7 (+ range validation): the truncated sorts
+// never run passes 0..P0-1, and the shared-memory atomics (one per key and digit)
+// bound this kernel.
+template <int DIM, int P0>
 __global__ void __launch_bounds__(256) hist_kernel(const int32_t* __restrict__ pts, uint32_t n,
                                                    uint32_t* __restrict__ g_hist, int* __restrict__ invalid, int4 sh2,
                                                    uint64_t* __restrict__ keys_out) {
-    __shared__ uint32_t sh[NPASS][256];
-    for (int i = threadIdx.x; i < NPASS * 256; i += 256) (&sh[0][0])[i] = 0;
+    constexpr int NP = NPASS - P0;
+    __shared__ uint32_t sh[NP][256];
+    for (int i = threadIdx.x; i < NP * 256; i += 256) (&sh[0][0])[i] = 0;
     __syncthreads();
     bool bad = false;
     for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < n; i += gridDim.x * 256) {
         uint64_t key = load_key_from_points<DIM>(pts, i, bad, sh2);
         keys_out[i] = key;   // the first pass reads these instead of re-encoding
 #pragma unroll
-        for (int p = 0; p < NPASS; ++p) atomicAdd(&sh[p][(key >> (8 * p)) & 255], 1u);
+        for (int p = P0; p < NPASS; ++p) atomicAdd(&sh[p - P0][(key >> (8 * p)) & 255], 1u);
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(invalid, 1);
-    for (int i = threadIdx.x; i < NPASS * 256; i += 256) {
+    for (int i = threadIdx.x; i < NP * 256; i += 256) {
         uint32_t v = (&sh[0][0])[i];
-        if (v) atomicAdd(g_hist + i, v);
+        if (v) atomicAdd(g_hist + P0 * 256 + i, v);
     }
 }
 
 __global__ void __launch_bounds__(256) scan_hist_kernel(const uint32_t* __restrict__ g_hist, uint32_t* __restrict__ offs) {
     __shared__ uint32_t s_warp[32];
-    for (int p = 0; p < NPASS; ++p) {
-        uint32_t v = g_hist[p * 256 + threadIdx.x];
-        offs[p * 256 + threadIdx.x] = block_exclusive_scan<256>(v, s_warp, nullptr);
-    }
+    const int p = blockIdx.x;   // one block per digit
+    uint32_t v = g_hist[p * 256 + threadIdx.x];
+    offs[p * 256 + threadIdx.x] = block_exclusive_scan<256>(v, s_warp, nullptr);
 }
 
 // MODE 0: first pass (encode points), 1: middle pass, 2: last pass (write records).
@@ -352,14 +354,24 @@ void sort_points_t(const int32_t* pts, int64_t n, uint32_t id_base, uint64_t* ke
         cudaEventRecord(pev[npev++], st);
     };
     mark();
-    cudaMemsetAsync(s.zero_block, 0, sort_zero_words(n) * sizeof(uint32_t), st);
+    if (approx || d_trunc_fail) {
+        // histograms and tile counters, then the look-back words of the passes that run
+        constexpr size_t P0 = kTruncBits / 8;
+        cudaMemsetAsync(s.zero_block, 0, (NPASS * 256 + NPASS) * sizeof(uint32_t), st);
+        cudaMemsetAsync(status + P0 * tiles * 256, 0, (NPASS - P0) * tiles * 256 * sizeof(uint32_t), st);
+    } else {
+        cudaMemsetAsync(s.zero_block, 0, sort_zero_words(n) * sizeof(uint32_t), st);
+    }
     mark();
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int hb = (int)std::min<size_t>((size_t)sms * 8, (n + 255) / 256);
-    hist_kernel<DIM><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid, psh, s.k[1]);
-    scan_hist_kernel<<<1, 256, 0, st>>>(hist, s.offs);
+    if (approx || d_trunc_fail)
+        hist_kernel<DIM, kTruncBits / 8><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid, psh, s.k[1]);
+    else
+        hist_kernel<DIM, 0><<<hb, 256, 0, st>>>(pts, un, hist, d_invalid, psh, s.k[1]);
+    scan_hist_kernel<<<NPASS, 256, 0, st>>>(hist, s.offs);
     mark();
     if (approx) {
         // order only by key bits 24..63 (digits 3..7); keys sharing those bits stay in
