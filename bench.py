@@ -250,18 +250,23 @@ def run_reference(args, D: Dist):
 # Alg. 3 + Alg. 2 on the same input) times the SASS cost of each operation as the k-NN
 # kernel implements it (scripts/op_costs.py -> profiles/r02_op_costs.json: distance
 # test per candidate, box test per child box, k-best insertion, ascent stop test).
-# Fallback (no file): the survey's hand estimates 9 / 22 / 30 / 15.
+# Fallback (no file): the survey's hand estimates.
 def _op_costs():
     try:
         d = json.loads((ROOT / "profiles" / "r02_op_costs.json").read_text())["ops"]
-        return ({k: d[k]["lane_instructions"] for k in ("dist", "box", "insert", "ascent")},
-                {k: d[k]["half_rate_instructions"] for k in ("dist", "box", "insert", "ascent")},
-                "profiles/r02_op_costs.json (cuobjdump -sass of scripts/op_costs.cu)")
+        # the final kernel's forms where the file has them (sign-bit hit masks, packed
+        # bf16 bound list), else the first round-2 forms
+        pick = {k: (k + "_final" if k + "_final" in d else k) for k in ("dist", "box", "insert", "ascent")}
+        return ({k: d[pick[k]]["lane_instructions"] for k in pick},
+                {k: d[pick[k]]["half_rate_instructions"] for k in pick},
+                "profiles/r02_op_costs.json (cuobjdump -sass of scripts/op_costs.cu; ops: " +
+                ", ".join(sorted(pick.values())) + ")")
     except Exception:
-        return (dict(dist=9, box=22, insert=3 * K_NN, ascent=15), dict(dist=0, box=0, insert=0, ascent=0),
-                "SURVEY §8(d) estimates")
+        return (dict(SURVEY_OP_COSTS), dict(dist=0, box=0, insert=0, ascent=0), "SURVEY §8(d) estimates")
 
 
+# SURVEY §8(d)'s hand estimates per operation (its ~2,670 thread-instructions per 3D query)
+SURVEY_OP_COSTS = dict(dist=10, box=20, insert=50, ascent=15)
 OP_COSTS, OP_HALF, OP_SOURCE = _op_costs()
 
 
@@ -273,8 +278,8 @@ def alu_ops_per_query(per_q: dict, costs: dict | None = None) -> float:
 
 def mix_peak_factor(per_q: dict) -> float:
     """Issue ceiling of the op mix relative to the full-rate one: half-rate
-    instructions (FMNMX, VIMNMX, IMAD.WIDE: 0.5 of full rate measured,
-    profiles/r01_alu_rates.json) occupy two issue slots' worth of their pipe."""
+    instructions (FMNMX, HMNMX2, PRMT, VIMNMX, IMAD.WIDE: 0.5 of full rate measured,
+    profiles/r01_alu_rates.json, r02_alu_rates_v2.json) occupy two issue slots' worth of their pipe."""
     tot = alu_ops_per_query(per_q)
     half = alu_ops_per_query(per_q, OP_HALF)
     return tot / (tot + half) if tot > 0 else 1.0
@@ -606,10 +611,14 @@ def knn_roofline(per_q: dict, nq: int, knn_ms: float, sm_max: float) -> dict:
     mixf = mix_peak_factor(per_q)
     return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "T lane-instr/s", "frac": achieved / peak,
             "peak_mix": peak * mixf, "frac_mix": achieved / (peak * mixf),
-            "ops_per_query": ops_q, "op_costs": OP_COSTS, "op_costs_half_rate": OP_HALF, "op_costs_source": OP_SOURCE,
+            "ops_per_query": ops_q,
+            # the same counters at SURVEY §8(d)'s hand-estimated costs (implementation-independent yardstick)
+            "ops_per_query_survey_costs": alu_ops_per_query(per_q, SURVEY_OP_COSTS),
+            "frac_survey_costs": alu_ops_per_query(per_q, SURVEY_OP_COSTS) * nq / (knn_ms / 1e3) / 1e12 / peak,
+            "op_costs": OP_COSTS, "op_costs_half_rate": OP_HALF, "op_costs_source": OP_SOURCE,
             "counters_per_query": per_q,
             "peak_note": "full-rate issue ceiling 148 SMs x 4 SMSPs x 32 lanes x sm_max clock (B200_PROFILING.md); "
-                         "peak_mix weights the op mix's half-rate FMNMX share (profiles/r01_alu_rates.json)",
+                         "peak_mix weights the op mix's half-rate share: FMNMX, HMNMX2, PRMT (profiles/r01_alu_rates.json, r02_alu_rates_v2.json)",
             "hbm_frac_compulsory": knn_bytes(nq) / (knn_ms / 1e3) / (HBM_PEAK_GBS * 1e9)}
 
 

@@ -17,12 +17,12 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 SRC = ROOT / "scripts" / "op_costs.cu"
-HALF_RATE = ("FMNMX", "VIMNMX", "IMNMX", "IMAD.WIDE")
-PER_STEP = {"op_dist4": 4}   # operations per loop iteration
+HALF_RATE = ("FMNMX", "VIMNMX", "IMNMX", "IMAD.WIDE", "HMNMX2", "PRMT")
+PER_STEP = {"op_dist4": 4, "op_dist4_final": 4}   # operations per loop iteration
 # per-iteration scaffolding of the microkernels that the product's loops do not have
 # (candidate index math + loop compare of op_dist4; the accumulator update of op_box
 # and op_ascent; the buffer-slot wrap of op_insert)
-SCAFFOLD = {"op_dist4": 4, "op_box": 3, "op_ascent": 3, "op_insert": 1}
+SCAFFOLD = {"op_dist4": 4, "op_dist4_final": 4, "op_box": 3, "op_ascent": 3, "op_insert": 1, "op_insert_final": 1}
 CONTROL = ("BRA", "BSSY", "BSYNC", "S2UR", "NOP", "LDCU", "EXIT")
 
 
@@ -66,7 +66,7 @@ def main():
         n = len(own) - SCAFFOLD.get(name, 0)
         half = sum(1 for o in own if o.startswith(HALF_RATE))
         k = PER_STEP.get(name, 1)
-        res[name.replace("op_", "").replace("dist4", "dist")] = {
+        res[name.replace("op_", "").replace("dist4", "dist")] = {   # dist, dist_final, box, insert, insert_final, ascent
             "lane_instructions": n / k, "half_rate_instructions": half / k, "loop_body": body}
     doc = {"source": "scripts/op_costs.cu (the product's expressions), cuobjdump -sass sm_100a: vector-pipe "
                      "instructions of each loop body, minus uniform-datapath bookkeeping, control flow and the "

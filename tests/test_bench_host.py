@@ -60,9 +60,12 @@ def test_alu_ops_model():
     c = bench.OP_COSTS
     assert bench.alu_ops_per_query(per_q) == pytest.approx(10 * c["dist"] + c["box"] + c["insert"] + c["ascent"])
     # SASS-derived costs are committed and sane: the insertion is the dearest op and
-    # carries the half-rate FMNMX chain (19 for k = 10)
-    assert bench.OP_SOURCE.startswith("profiles/")
-    assert c["insert"] > c["box"] > c["dist"] > 0 and bench.OP_HALF["insert"] == 19
+    # carries the half-rate chain (k = 10: 10 HMNMX2 + 5 PRMT for the packed bf16 list)
+    assert bench.OP_SOURCE.startswith("profiles/") and "insert_final" in bench.OP_SOURCE
+    assert c["insert"] > c["box"] > c["dist"] > 0 and bench.OP_HALF["insert"] == 15
+    # SURVEY §8(d)'s fixed yardstick: ~2,670 thread-instructions per 3D query at its counts
+    assert bench.alu_ops_per_query(dict(dist_evals=92.3, box_tests=48.1, replacements=13.0, ascents=9.3),
+                                   bench.SURVEY_OP_COSTS) == pytest.approx(2670, rel=0.01)
     assert 0.5 < bench.mix_peak_factor(dict(dist_evals=92, box_tests=45, ascents=9, replacements=23)) < 1.0
 
 
