@@ -1090,7 +1090,9 @@ struct PacketArgs {
 #define ZD_PCHUNK 1      // packets per fetch of a persistent warp
 #endif
 #ifndef ZD_INCOHERENT
-#define ZD_INCOHERENT 4096.0f   // defer a packet if its extent^2 > this * median bound
+#define ZD_INCOHERENT 65536.0f  // defer a packet if its extent^2 > this * median bound (retuned under the
+                                // persistent first pass: 4096 deferred ~500 packets at C2 / C4b, whose one-query-
+                                // per-warp second launch cost more than searching them as packets)
 #endif
 
 
