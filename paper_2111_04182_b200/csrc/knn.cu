@@ -283,14 +283,23 @@ __device__ __forceinline__ void stf(WarpSh<DIM, K>& S, int j, float4 v) {
 constexpr int kSeedW = ZD_SEEDW;
 
 // The ascending list fa of the k smallest candidate upper bounds seen so far (only
-// fa[K-1], the bound, is ever read).  Even K: packed bf16 pairs, every value rounded
+// fa[K-1], the bound, is ever read).  Even K <= 10: packed bf16 pairs, every value rounded
 // UP to bf16 (monotone, so fa[K-1] is the bf16 round-up of the fp32 list's last entry:
 // a bound at most 2^-8 looser, never tighter); the median insertion then takes two
 // HMNMX2 and one PRMT per pair instead of four FMNMX, in half the registers.
+// The packed list resolves the bound to 2^-7 only.  A lane whose candidates are far and
+// nearly equidistant (relative spread below one bf16 step: an outlier looking at a distant
+// dense cluster, a root-based search before its lists settle, the larger bounds of K >=
+// 16) then takes EVERY such candidate as a hit instead of the ~K ln N record-breakers:
+// measured at 10M points, k = 16 on the Plummer sphere 189 ms instead of 15 ms, root-based
+// k = 10 on the 2D Kuzmin disk 9.3 s instead of 19 ms.  So it is used only for K <= 10 in
+// leaf-based searches, where the window seed bounds every lane by its 24 Morton
+// neighbours first (all five 10M datasets: within the fp32 list's time or 1-8% faster);
+// root-based searches with 1 < k <= 10 run on the K = 11 instantiation (fp32 list).
 #ifndef ZD_FA_BF16
 #define ZD_FA_BF16 1
 #endif
-template <int K, bool PACK = (ZD_FA_BF16 && K % 2 == 0)>
+template <int K, bool PACK = (ZD_FA_BF16 && K % 2 == 0 && K <= 10)>
 struct FaList {
     float v[K];
     __device__ __forceinline__ void init() {
@@ -463,6 +472,53 @@ __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Qu
             rank += (dv < de || (dv == de && cf.w < ce.w)) ? 1 : 0;
         }
         if (rank >= K) S.be[e][lane].y = __float_as_int(INFINITY);
+    }
+}
+
+// Second-level compaction for a lane whose buffer is still full after compact(): drop
+// every entry above the K-th smallest buffered upper bound B (the buffer holds every
+// candidate that can still be a final neighbour, so an entry with ub > B — 3D: > B (1 +
+// 2^-20), the slack of the fp32-derived bounds — has K strictly closer candidates).
+// This is the cut an exact fp32 bound list would make.  The packed bf16 list resolves
+// bounds only to 2^-7: a lane that is far from the candidates it is seeing (an
+// incoherent packet that was not deferred, a root-based search before its lists settle)
+// gets whole spans inside one bf16 step of its bound, and without this cut each overflow
+// fell through to mark_exact_losers (O(cnt^2) record loads): C2 root-based k = 10 ran
+// 361 ms instead of 10 ms; with it, and with the packed list kept to K <= 10 leaf-based
+// searches (FaList), the rare crowded lane costs one O(cnt^2) pass over its own column.
+template <int DIM, int K>
+__device__ __noinline__ int tight_compact(int cnt, WarpSh<DIM, K>& S, int lane) {
+    float B = INFINITY;
+    for (int e = 0; e < cnt; ++e) {
+        const float ue = __int_as_float(S.be[e][lane].y);
+        int rank = 0;
+        for (int f = 0; f < cnt; ++f) {
+            const float uf = __int_as_float(S.be[f][lane].y);
+            rank += (uf < ue || (uf == ue && f < e)) ? 1 : 0;
+        }
+        if (rank == K - 1) B = ue;
+    }
+    const float F = DIM == 3 ? __fmul_ru(B, 1.0f + 0x1p-20f) : B;
+    int w = 0;
+    for (int e = 0; e < cnt; ++e) {
+        const int2 v = S.be[e][lane];
+        S.be[w][lane] = v;
+        w += (__int_as_float(v.y) <= F) ? 1 : 0;
+    }
+    return w;
+}
+
+// A full buffer must take one more entry: compact by the lane's bound, then by the K-th
+// smallest buffered bound, and only on true massive ties rank the survivors exactly.
+template <int DIM, int K>
+__device__ __forceinline__ void make_room(const int4* __restrict__ recs, Lane<DIM, K>& L, WarpSh<DIM, K>& S, int lane) {
+    compact<DIM, K>(L, S, lane);
+    if (L.cnt == Cap<DIM, K>::v) {
+        L.cnt = tight_compact<DIM, K>(L.cnt, S, lane);
+        if (L.cnt == Cap<DIM, K>::v) {   // massive ties: keep only the exact K best
+            mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
+            compact<DIM, K>(L, S, lane);
+        }
     }
 }
 
@@ -782,13 +838,7 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
 #endif
                 L.fa.insert(xf);
                 set_bound<DIM, K>(L);
-                if (L.cnt == Cap<DIM, K>::v) {   // rare: per-lane compaction
-                    compact<DIM, K>(L, S, lane);
-                    if (L.cnt == Cap<DIM, K>::v) {   // massive ties: keep only the exact K best
-                        mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
-                        compact<DIM, K>(L, S, lane);
-                    }
-                }
+                if (L.cnt == Cap<DIM, K>::v) make_room<DIM, K>(recs, L, S, lane);   // rare: per-lane compaction
                 ZD_DCHECK((L.cnt < Cap<DIM, K>::v));
                 S.be[L.cnt][lane] = make_int2(S.p[j], __float_as_int(xf));
                 ++L.cnt;
@@ -864,13 +914,7 @@ __device__ __forceinline__ void seed_scan(const int4* __restrict__ recs, int32_t
                         cid = c.w;
                     }
                     if (in && cid != L.q.id) {
-                        if (L.cnt == Cap<DIM, K>::v) {   // rare (ties): keep the exact K best
-                            compact<DIM, K>(L, S, lane);
-                            if (L.cnt == Cap<DIM, K>::v) {
-                                mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
-                                compact<DIM, K>(L, S, lane);
-                            }
-                        }
+                        if (L.cnt == Cap<DIM, K>::v) make_room<DIM, K>(recs, L, S, lane);   // rare (ties)
                         S.be[L.cnt][lane] = make_int2(b + j, __float_as_int(xf));
                         ++L.cnt;
                     }
@@ -937,13 +981,7 @@ __device__ __forceinline__ void window_seed(const int4* __restrict__ recs, int32
                 if (!valid) xf = INFINITY;
                 if (__any_sync(0xffffffffu, xf < L.fa.last())) L.fa.insert(xf);
             } else if (valid && in) {
-                if (L.cnt == Cap<DIM, K>::v) {   // rare (ties): keep the exact K best
-                    compact<DIM, K>(L, S, lane);
-                    if (L.cnt == Cap<DIM, K>::v) {
-                        mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
-                        compact<DIM, K>(L, S, lane);
-                    }
-                }
+                if (L.cnt == Cap<DIM, K>::v) make_room<DIM, K>(recs, L, S, lane);   // rare (ties)
                 S.be[L.cnt][lane] = make_int2(base + lane + j, __float_as_int(xf));
                 ++L.cnt;
             }
@@ -1094,6 +1132,10 @@ struct PacketArgs {
                                 // persistent first pass: 4096 deferred ~500 packets at C2 / C4b, whose one-query-
                                 // per-warp second launch cost more than searching them as packets)
 #endif
+#ifndef ZD_INCOHERENT16
+#define ZD_INCOHERENT16 4096.0f // the same for K >= 16, where the joint search of a spread-out packet costs more
+                                // (measured: K2 k = 16 11.9 ms at 4096, 17.7 ms at 16384 and 65536)
+#endif
 
 
 // EXT = false: all-points (queries are the tree's own points; self excluded by id,
@@ -1240,7 +1282,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
             }
         }
         const float med = __shfl_sync(0xffffffffu, v, nact >> 1);
-        if (A.defer_all || (nfin == nact && ext2 > ZD_INCOHERENT * exp2f(med))) {
+        if (A.defer_all || (nfin == nact && ext2 > (K <= 10 ? ZD_INCOHERENT : ZD_INCOHERENT16) * exp2f(med))) {
             int slot = 0;
             if (lane == 0) slot = atomicAdd(A.hard_count, 1);
             slot = __shfl_sync(0xffffffffu, slot, 0);
@@ -1418,7 +1460,7 @@ __device__ __forceinline__ bool search_packet(const PacketArgs& A, int32_t p0, i
 }
 
 template <int DIM, int K, bool EXT>
-__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 10 ? (DIM == 3 ? ZD_MINB3 : ZD_MINB)
+__global__ void __launch_bounds__(Pw<K>::v * 32, (K <= 11 ? (DIM == 3 ? ZD_MINB3 : ZD_MINB)
                                                     : (K <= 16 ? (DIM == 3 ? ZD_MINB16_3 : ZD_MINB16)
                                                                : (DIM == 3 ? ZD_MINB32_3 : ZD_MINB32)))) knn_packet_kernel(PacketArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1546,6 +1588,8 @@ void launch_packets(const PacketArgs& A, cudaStream_t st) {
 
 template <int DIM, bool EXT>
 void dispatch(const PacketArgs& A, cudaStream_t st) {
+    // root-based searches (ablation) keep the fp32 bound list: K = 1, else the odd K = 11
+    if (A.root_based && A.k > 1 && A.k <= 11) { launch_packets<DIM, 11, EXT>(A, st); return; }
 #define X(KK) if (A.k <= KK) { launch_packets<DIM, KK, EXT>(A, st); return; }
     ZD_K_CASES(X)
 #undef X
