@@ -129,3 +129,36 @@ def test_config_full_shift_3d(zd, oracle_mod):
     assert bad.size == 0, f"{bad.size} rows differ"
     st = oracle_mod.Tree(pts, shift=sh)
     assert t.zd_get_info()["n_internal"] == (st.nodes()["split"] >= 0).sum()
+
+
+@pytest.mark.parametrize("dist,dim", [("kuzmin", 2), ("plummer", 3)])
+def test_time_sanity_across_k_and_root_based(zd, dist, dim):
+    """Guards the search's work bound, not its answers: on heavy-tailed data (outliers
+    looking at a distant dense core) a bound list that cannot separate nearly equidistant
+    candidates makes every one of them a hit.  With the packed bf16 list at every even K
+    this ran 100-2000x slower than at k = 10 (2D Kuzmin, 10M: k = 16 9.1 s, root-based k =
+    10 9.3 s against 4.7 ms).  Normal ratios to the leaf-based k = 10
+    time: root-based ~4x, k = 16 ~2.5x, k = 32 ~10x; the limits leave a wide margin."""
+    n = 4_000_000
+    t = zd.zd_build(torch.from_numpy(zdgen.points(dist, n, dim, seed=9)).cuda())
+
+    def ms(k, root):
+        oi = torch.empty((n, k), dtype=torch.int32, device="cuda")
+        od = torch.empty((n, k), dtype=torch.int64, device="cuda")
+        best = None
+        for _ in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            t.zd_knn(k, out_idx=oi, out_dist2=od, root_based=root)
+            e1.record()
+            torch.cuda.synchronize()
+            best = e0.elapsed_time(e1) if best is None else min(best, e0.elapsed_time(e1))
+        return best
+
+    base = ms(10, False)
+    assert ms(10, True) < 20 * base
+    assert ms(4, True) < 20 * base
+    assert ms(16, False) < 12 * base
+    assert ms(32, False) < 50 * base
+    assert ms(1, False) < 2 * base
+    t.zd_free()
