@@ -250,6 +250,23 @@ constexpr int kPG = ZD_PREGROUPS, kPGW = 32 / ZD_PREGROUPS;
 #ifndef ZD_PREFILTER2D
 #define ZD_PREFILTER2D 0 // the same in 2D (exact int64; measured slightly slower on C2 / 2D Kuzmin)
 #endif
+// The packed list resolves the bound to 2^-7 only.  A lane whose candidates are far and
+// nearly equidistant (relative spread below one bf16 step: an outlier looking at a distant
+// dense cluster, a root-based search before its lists settle, the larger bounds of K >=
+// 16) then takes EVERY such candidate as a hit instead of the ~K ln N record-breakers:
+// measured at 10M points, k = 16 on the Plummer sphere 189 ms instead of 15 ms, root-based
+// k = 10 on the 2D Kuzmin disk 9.3 s instead of 19 ms.  So it is used only for K <= 10 in
+// leaf-based searches, where the window seed bounds every lane by its 24 Morton
+// neighbours first (all five 10M datasets: within the fp32 list's time or 1-8% faster);
+// root-based searches with 1 < k <= 10 run on the K = 11 instantiation (fp32 list).
+#ifndef ZD_FA_BF16
+#define ZD_FA_BF16 1
+#endif
+#ifndef ZD_FA_BF16_MAXK
+#define ZD_FA_BF16_MAXK 10   // (32 reproduces the regression for tests/test_gpu_fullsize.py's time guard)
+#endif
+template <int K>
+constexpr bool kPackedFa = ZD_FA_BF16 && K % 2 == 0 && K <= ZD_FA_BF16_MAXK;
 template <int DIM, int K>
 struct WarpSh {
     int4 c[DIM == 2 ? 32 : 1];           // 2D: staged candidates (x, y, 0, id)
@@ -287,22 +304,7 @@ constexpr int kSeedW = ZD_SEEDW;
 // UP to bf16 (monotone, so fa[K-1] is the bf16 round-up of the fp32 list's last entry:
 // a bound at most 2^-8 looser, never tighter); the median insertion then takes two
 // HMNMX2 and one PRMT per pair instead of four FMNMX, in half the registers.
-// The packed list resolves the bound to 2^-7 only.  A lane whose candidates are far and
-// nearly equidistant (relative spread below one bf16 step: an outlier looking at a distant
-// dense cluster, a root-based search before its lists settle, the larger bounds of K >=
-// 16) then takes EVERY such candidate as a hit instead of the ~K ln N record-breakers:
-// measured at 10M points, k = 16 on the Plummer sphere 189 ms instead of 15 ms, root-based
-// k = 10 on the 2D Kuzmin disk 9.3 s instead of 19 ms.  So it is used only for K <= 10 in
-// leaf-based searches, where the window seed bounds every lane by its 24 Morton
-// neighbours first (all five 10M datasets: within the fp32 list's time or 1-8% faster);
-// root-based searches with 1 < k <= 10 run on the K = 11 instantiation (fp32 list).
-#ifndef ZD_FA_BF16
-#define ZD_FA_BF16 1
-#endif
-#ifndef ZD_FA_BF16_MAXK
-#define ZD_FA_BF16_MAXK 10   // (32 reproduces the regression for tests/test_gpu_fullsize.py's time guard)
-#endif
-template <int K, bool PACK = (ZD_FA_BF16 && K % 2 == 0 && K <= ZD_FA_BF16_MAXK)>
+template <int K, bool PACK = kPackedFa<K>>
 struct FaList {
     float v[K];
     __device__ __forceinline__ void init() {
@@ -359,8 +361,7 @@ struct Lane {
 };
 
 template <int DIM, int K>
-__device__ __forceinline__ void set_bound(Lane<DIM, K>& L) {
-    const float f = L.fa.last();
+__device__ __forceinline__ void set_bound_from(Lane<DIM, K>& L, float f) {
     if (DIM == 3) {
         // 3D: coordinates and their differences are exact in fp32 and the three rounded
         // products/sums make the fp32 d2 at most (1 + 3.0000002 * 2^-24) times the
@@ -368,6 +369,21 @@ __device__ __forceinline__ void set_bound(Lane<DIM, K>& L) {
         L.wb = __fmul_ru(f, 1.0f + 0x1p-21f);
     } else {
         L.U = (f == INFINITY) ? INT64_MAX : __float2ll_ru(f);
+    }
+}
+template <int DIM, int K>
+__device__ __forceinline__ void set_bound(Lane<DIM, K>& L) {
+    set_bound_from<DIM, K>(L, L.fa.last());
+}
+// the same, never loosening the bound (packed list after tighten(): the test bound may
+// already be tighter than the list's bf16 last entry)
+template <int DIM, int K>
+__device__ __forceinline__ void lower_bound_to(Lane<DIM, K>& L, float f) {
+    if (DIM == 3) {
+        L.wb = fminf(L.wb, __fmul_ru(f, 1.0f + 0x1p-21f));
+    } else {
+        const int64_t u = (f == INFINITY) ? INT64_MAX : __float2ll_ru(f);
+        L.U = u < L.U ? u : L.U;
     }
 }
 
@@ -446,7 +462,12 @@ template <int DIM, int K>
 __device__ __forceinline__ void compact(Lane<DIM, K>& L, WarpSh<DIM, K>& S, int lane) {
     // 3D buffers fp32-derived upper bounds ub with d2 <= ub <= d2 (1 + 2^-20): a final
     // neighbour has ub <= D_k (1 + 2^-20) <= fa[K-1] (1 + 2^-20)
-    const float F = DIM == 3 ? __fmul_ru(L.fa.last(), 1.0f + 0x1p-20f) : L.fa.last();
+    // packed list: the cut comes from the lane's test bound, which only decreases and may
+    // be tighter than the list's last entry (tighten): wb >= fK (1 + 2^-21) and U >= fK for
+    // the true K-th smallest upper bound fK, so F >= fK (1 + 2^-20) resp. F >= fK as below
+    float F;
+    if constexpr (kPackedFa<K>) F = DIM == 3 ? __fmul_ru(L.wb, 1.0f + 0x1p-21f) : __ll2float_ru(L.U);
+    else F = DIM == 3 ? __fmul_ru(L.fa.last(), 1.0f + 0x1p-20f) : L.fa.last();
     int w = 0;
     for (int e = 0; e < L.cnt; ++e) {
         const int2 v = S.be[e][lane];
@@ -490,7 +511,7 @@ __device__ __noinline__ void mark_exact_losers(const int4* __restrict__ recs, Qu
 // 361 ms instead of 10 ms; with it, and with the packed list kept to K <= 10 leaf-based
 // searches (FaList), the rare crowded lane costs one O(cnt^2) pass over its own column.
 template <int DIM, int K>
-__device__ __noinline__ int tight_compact(int cnt, WarpSh<DIM, K>& S, int lane) {
+__device__ __noinline__ int2 tight_compact(int cnt, WarpSh<DIM, K>& S, int lane) {
     float B = INFINITY;
     for (int e = 0; e < cnt; ++e) {
         const float ue = __int_as_float(S.be[e][lane].y);
@@ -508,7 +529,18 @@ __device__ __noinline__ int tight_compact(int cnt, WarpSh<DIM, K>& S, int lane) 
         S.be[w][lane] = v;
         w += (__int_as_float(v.y) <= F) ? 1 : 0;
     }
-    return w;
+    return make_int2(w, __float_as_int(B));   // (new count, the K-th smallest buffered upper bound)
+}
+
+// Exact cut of a crowded buffer; with the packed list the K-th smallest buffered bound
+// also lowers the lane's test bound (wb / U, which from then on only decrease), so that
+// the candidates inside the same bf16 step stop being hits.  It is the value an exact
+// fp32 list would hold, so the bound stays as sound as the list's last entry.
+template <int DIM, int K>
+__device__ __forceinline__ void tighten(Lane<DIM, K>& L, WarpSh<DIM, K>& S, int lane) {
+    const int2 r = tight_compact<DIM, K>(L.cnt, S, lane);
+    L.cnt = r.x;
+    if constexpr (kPackedFa<K>) lower_bound_to<DIM, K>(L, __int_as_float(r.y));
 }
 
 // A full buffer must take one more entry: compact by the lane's bound, then by the K-th
@@ -517,7 +549,7 @@ template <int DIM, int K>
 __device__ __forceinline__ void make_room(const int4* __restrict__ recs, Lane<DIM, K>& L, WarpSh<DIM, K>& S, int lane) {
     compact<DIM, K>(L, S, lane);
     if (L.cnt == Cap<DIM, K>::v) {
-        L.cnt = tight_compact<DIM, K>(L.cnt, S, lane);
+        tighten<DIM, K>(L, S, lane);
         if (L.cnt == Cap<DIM, K>::v) {   // massive ties: keep only the exact K best
             mark_exact_losers<DIM, K>(recs, L.q, L.cnt, S, lane);
             compact<DIM, K>(L, S, lane);
@@ -528,6 +560,9 @@ __device__ __forceinline__ void make_room(const int4* __restrict__ recs, Lane<DI
 // Every lane scans sorted positions [s, e): up to 32 records at a time are staged
 // through shared memory, each lane tests CH of them per uniform pass against its
 // bound, then handles its (few) hits.
+#ifndef ZD_CROWD
+#define ZD_CROWD 3          // packed list: lanes left with more than K + CROWD entries by a uniform compaction take the exact cut
+#endif
 #ifndef ZD_SLACK
 #define ZD_SLACK 2          // uniform compaction when a needing lane has > CAP - SLACK entries (2: measured best of 0-6)
 #endif
@@ -637,6 +672,11 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
             if (__any_sync(0xffffffffu, need && L.cnt > Cap<DIM, K>::v - ZD_SLACK)) {
                 ZD_STAT(ZS_COMPACT, 1);
                 compact<DIM, K>(L, S, lane);
+                // packed list: a buffer still crowded after the cut by the lane's bound holds
+                // candidates inside one bf16 step of it (far, nearly equidistant points)
+                if constexpr (kPackedFa<K>) {
+                    if (L.cnt > K + ZD_CROWD) tighten<DIM, K>(L, S, lane);
+                }
             }
             uint32_t hit = 0;
             if (w > TMax<DIM>::v) {
@@ -840,7 +880,8 @@ __device__ __forceinline__ void scan_span(const int4* __restrict__ recs, int32_t
                 if (L.cnt == Cap<DIM, K>::v) atomicAdd(&g_knn_stats[ZS_LANE_COMPACT], 1ull);
 #endif
                 L.fa.insert(xf);
-                set_bound<DIM, K>(L);
+                if constexpr (kPackedFa<K>) lower_bound_to<DIM, K>(L, L.fa.last());
+                else set_bound<DIM, K>(L);
                 if (L.cnt == Cap<DIM, K>::v) make_room<DIM, K>(recs, L, S, lane);   // rare: per-lane compaction
                 ZD_DCHECK((L.cnt < Cap<DIM, K>::v));
                 S.be[L.cnt][lane] = make_int2(S.p[j], __float_as_int(xf));

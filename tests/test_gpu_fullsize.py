@@ -162,3 +162,34 @@ def test_time_sanity_across_k_and_root_based(zd, dist, dim):
     assert ms(32, False) < 50 * base
     assert ms(1, False) < 2 * base
     t.zd_free()
+
+
+def test_time_sanity_far_dense_cluster(zd, oracle_mod):
+    """64 outliers whose 10 nearest neighbours are points of a distant dense cluster at
+    nearly equal distances (relative spread below the packed bf16 bound list's 2^-7
+    step): with the list alone every cluster point was a hit for them (230 ms at 2M
+    points against 1.9 ms with an fp32 list); the exact cut of crowded buffers
+    (tight_compact, knn.cu) bounds it.  Also checks the outliers' rows vs brute force."""
+    n, m = 2_000_000, 64
+    rng = np.random.default_rng(3)
+    c = 1 << 20
+    core = rng.normal(0.0, 600.0, size=(n - m, 3))
+    v = rng.normal(size=(m, 3))
+    v /= np.linalg.norm(v, axis=1, keepdims=True)
+    pts = np.clip(np.rint(np.concatenate([core, v * (0.9 * c)]) + c), 0, (1 << 21) - 1).astype(np.int32)
+    t = zd.zd_build(torch.from_numpy(pts).cuda())
+    oi = torch.empty((n, K), dtype=torch.int32, device="cuda")
+    od = torch.empty((n, K), dtype=torch.int64, device="cuda")
+    best = None
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        t.zd_knn(K, out_idx=oi, out_dist2=od)
+        e1.record()
+        torch.cuda.synchronize()
+        best = e0.elapsed_time(e1) if best is None else min(best, e0.elapsed_time(e1))
+    assert best < 25.0, f"far-cluster k-NN took {best:.1f} ms"
+    rows = np.arange(n - m, n)
+    bi, bd = oracle_mod.brute_knn(pts, None, pts[rows], rows.astype(np.int32), K)   # self excluded by id
+    assert np.array_equal(oi[rows].cpu().numpy(), bi) and np.array_equal(od[rows].cpu().numpy(), bd)
+    t.zd_free()
