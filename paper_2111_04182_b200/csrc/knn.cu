@@ -257,8 +257,13 @@ constexpr int kPG = ZD_PREGROUPS, kPGW = 32 / ZD_PREGROUPS;
 // measured at 10M points, k = 16 on the Plummer sphere 189 ms instead of 15 ms, root-based
 // k = 10 on the 2D Kuzmin disk 9.3 s instead of 19 ms.  So it is used only for K <= 10 in
 // leaf-based searches, where the window seed bounds every lane by its 24 Morton
-// neighbours first (all five 10M datasets: within the fp32 list's time or 1-8% faster);
+// neighbours first (all five 10M datasets: within the fp32 list's time or 1-7% faster);
 // root-based searches with 1 < k <= 10 run on the K = 11 instantiation (fp32 list).
+// And even there a constructed input (outliers whose k nearest neighbours are a distant
+// dense cluster) hit the same cliff, so the packed list is backed by exact cuts: the
+// lane's test bound only decreases (lower_bound_to), and a buffer that stays crowded
+// after the cut by that bound is cut at its exact K-th smallest buffered bound, which
+// also lowers the test bound (tighten) — the value an fp32 list would hold.
 #ifndef ZD_FA_BF16
 #define ZD_FA_BF16 1
 #endif
